@@ -1,0 +1,449 @@
+"""bench.py — throughput of the paper's BLAS hot path on B200 (driver contract).
+
+One STEP = one pass of every §8(a) row over one batch of synthetic input, per rank:
+    scal  y = 3*x,            n = 2^28   (BASELINE configs[2], Fig. 3's mul3)
+    asum  sum|x|,             n = 2^28   (configs[2])
+    dot   sum x*y,            n = 2^26   (configs[1], large case)
+    gemv  1.5*A@x + 0.5*y,    8192 x 8192 rows per rank (configs[3])
+  + X1 at N > 1: all-gather of the asum/dot fp64 partials + lift_combine, and
+    all-gather of the gemv y slices (weak scaling: rank r owns global slice r).
+metric = achieved HBM GB/s = algorithmic bytes of the step
+         / device time.  Every operand is >= 256 MiB > the 126 MB L2, so no flush.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lift|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+N_VEC = 1 << 28      # scal / asum
+N_DOT = 1 << 26      # dot
+GEMV_M = 8192        # rows per rank
+GEMV_N = 8192
+ALPHA_SCAL = 3.0
+ALPHA, BETA = 1.5, 0.5
+NOMINAL_HBM = 8000.0  # GB/s, BASELINE.json's denominator (nominal)
+
+OPS = ("scal", "asum", "dot", "gemv")
+
+
+def op_bytes(world: int = 1) -> dict:
+    """Algorithmic bytes per launch (per rank): what the op must move."""
+    return {
+        "scal": 8 * N_VEC,                                  # read x + write y
+        "asum": 4 * N_VEC,                                  # read x
+        "dot": 8 * N_DOT,                                   # read x, y
+        "gemv": 4 * (GEMV_M * GEMV_N + GEMV_N + 2 * GEMV_M),  # A, x, y in, y_out
+    }
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """Per-launch dram bytes from the committed ncu --set full capture, if present."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self, t0, t1):
+        rows = [r for (t, r) in self.rows if t0 <= t <= t1] or [r for (_, r) in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[2:]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------- oracle arm
+def oracle_sample(frac_shift: int):
+    """Host inputs for a bounded sample of one step: every op at 1/2^frac_shift size."""
+    import lift_inputs as gen
+    ns, nd, gm = N_VEC >> frac_shift, N_DOT >> frac_shift, max(1, GEMV_M >> frac_shift)
+    return {
+        "x": gen.host(ns, 0, gen.TID_X),
+        "dx": gen.host(nd, 0, gen.TID_X, lo=0.0, hi=1.0),
+        "dy": gen.host(nd, 0, gen.TID_Y, lo=0.0, hi=2.0),
+        "A": gen.host(gm * GEMV_N, 0, gen.TID_A, lo=0.0, hi=3.0).reshape(gm, GEMV_N),
+        "gx": gen.host(GEMV_N, 0, gen.TID_X, lo=0.0, hi=1.0),
+        "gy": gen.host(gm, 0, gen.TID_Y, lo=0.0, hi=2.0),
+        "bytes": 12 * ns + 8 * nd + 4 * (gm * GEMV_N + GEMV_N + 2 * gm),
+        "desc": (f"one step at 1/{1 << frac_shift} size: scal+asum n=2^{28 - frac_shift}, "
+                 f"dot n=2^{26 - frac_shift}, gemv {gm}x{GEMV_N}"),
+    }
+
+
+def oracle_step(s):
+    import oracle
+    oracle.scal(ALPHA_SCAL, s["x"])
+    oracle.asum(s["x"])
+    oracle.dot(s["dx"], s["dy"])
+    oracle.gemv(s["A"], s["gx"], s["gy"], ALPHA, BETA)
+
+
+def cpu_baseline(budget_s: float = 10.0, frac_shift: int = 3):
+    """The oracle as it stands, single-threaded, on a bounded sample (rank 0, N=1)."""
+    s = oracle_sample(frac_shift)
+    oracle_step(s)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle_step(s)
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(s["bytes"] * reps / dt / 1e9, 3), "unit": "GB/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{reps} x ({s['desc']}) in {dt:.1f} s, fp64 Neumaier C oracle, 1 thread"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0  # under torchrun only rank 0 runs the CPU oracle
+    frac_shift = 4
+    s = oracle_sample(frac_shift)
+    for _ in range(args.warmup):
+        oracle_step(s)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(s)
+    dt = time.perf_counter() - t0
+    val = s["bytes"] * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "achieved HBM GB/s (fraction of 8 TB/s) for "
+        "asum/dot/scal/gemv at 1/2/4/8 B200", "value": round(val, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "scal+asum 2^28, dot 2^26, gemv 8192x8192 (sampled 1/16)",
+                   "global_batch": 1, "parallelism": "cpu-1thread"},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": s["desc"]},
+        "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------- lift arm
+def run_lift(args):
+    import torch
+    import torch.distributed as dist
+
+    import lift_inputs as gen
+    import paper_1502_02389_b200 as lift
+    from paper_1502_02389_b200 import dist as ldist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    group = None
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs, resident in HBM (rank r owns global slice r: weak scaling) ----------
+    def fill(n, tid, i0, lo, hi):
+        t = torch.empty(n, dtype=torch.float32, device=dev)
+        return gen.fill_device(t, 0, tid, i0, gen.DIST_UNIFORM, lo, hi)
+
+    x_v = fill(N_VEC, gen.TID_X, rank * N_VEC, -1.0, 1.0)
+    y_v = torch.empty(N_VEC, dtype=torch.float32, device=dev)
+    x_d = fill(N_DOT, gen.TID_X, rank * N_DOT, 0.0, 1.0)
+    y_d = fill(N_DOT, gen.TID_Y, rank * N_DOT, 0.0, 2.0)
+    A = fill(GEMV_M * GEMV_N, gen.TID_A, rank * GEMV_M * GEMV_N, 0.0, 3.0).view(GEMV_M, GEMV_N)
+    g_x = fill(GEMV_N, gen.TID_X, 0, 0.0, 1.0)  # replicated
+    g_y = fill(GEMV_M, gen.TID_Y, rank * GEMV_M, 0.0, 2.0)
+    g_out = torch.empty(GEMV_M, dtype=torch.float32, device=dev)
+    g_full = torch.empty(GEMV_M * world, dtype=torch.float32, device=dev)
+    r_asum = torch.empty(1, dtype=torch.float32, device=dev)
+    r_dot = torch.empty(1, dtype=torch.float32, device=dev)
+    ws_a = lift.Workspace(N_VEC, dev)
+    ws_d = lift.Workspace(N_DOT, dev)
+    torch.cuda.synchronize()
+
+    def step(ev=None):
+        """One pass of the hot path; ev = per-op (start, end) event pairs or None."""
+        def rec(i):
+            if ev is not None:
+                ev[i].record(stream)
+        rec(0)
+        lift.scal(ALPHA_SCAL, x_v, out=y_v)
+        rec(1)
+        if world == 1:
+            lift.asum(x_v, out=r_asum, ws=ws_a)
+        else:
+            ldist.sharded_asum(x_v, group, out=r_asum, ws=ws_a)
+        rec(2)
+        if world == 1:
+            lift.dot(x_d, y_d, out=r_dot, ws=ws_d)
+        else:
+            ldist.sharded_dot(x_d, y_d, group, out=r_dot, ws=ws_d)
+        rec(3)
+        if world == 1:
+            lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out)
+        else:
+            ldist.sharded_gemv(A, g_x, g_y, ALPHA, BETA, GEMV_M * world, group,
+                               out_full=g_full, out_slice=g_out)
+        rec(4)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    barrier()
+
+    # ---- timed region: K steps, per-op events on the launching stream ---------------
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    barrier()
+    t_wall0 = time.time()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    end.record(stream)
+    barrier()
+    t_wall1 = time.time()
+    # keep the GPU busy until the sampler has seen the load (short K on a fast GPU)
+    while sampler and len([1 for (t, _) in sampler.rows if t >= t_wall0]) < 5 \
+            and time.time() - t_wall0 < 10:
+        step()
+        torch.cuda.synchronize()
+    t_wall2 = time.time()
+    if sampler:
+        sampler.stop()
+    total_ms = max_over_ranks(start.elapsed_time(end))
+    per_op_ms = {op: 0.0 for op in OPS}
+    for k in range(args.steps):
+        for i, op in enumerate(OPS):
+            per_op_ms[op] += evs[k][i].elapsed_time(evs[k][i + 1])
+    per_op_ms = {op: max_over_ranks(v) / args.steps for op, v in per_op_ms.items()}
+
+    ob = op_bytes(world)
+    step_bytes = sum(ob.values())
+    ms_per_step = total_ms / args.steps
+    value = step_bytes * world / (ms_per_step * 1e-3) / 1e9  # whole-job GB/s
+
+    # ---- e2e: the same step through the public API with pinned HOST buffers --------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
+                      max_over_ranks, barrier, step_bytes)
+
+    peak, peak_src = load_peaks()
+    traffic = load_traffic()
+    dom = max(OPS, key=lambda o: per_op_ms[o])
+    dom_gbs = ob[dom] / (per_op_ms[dom] * 1e-3) / 1e9
+    per_op = {op: {"ms": round(per_op_ms[op], 4), "bytes": ob[op],
+                   "GB/s": round(ob[op] / (per_op_ms[op] * 1e-3) / 1e9, 1),
+                   "frac_measured_peak": round(ob[op] / (per_op_ms[op] * 1e-3) / 1e9 / peak, 4),
+                   "frac_8TBs": round(ob[op] / (per_op_ms[op] * 1e-3) / 1e9 / NOMINAL_HBM, 4),
+                   "share_of_step": round(per_op_ms[op] / ms_per_step, 4)}
+              for op in OPS}
+
+    if rank == 0:
+        launches_per_step = 4 + (2 if world > 1 else 0)
+        line = {
+            "metric": "achieved HBM GB/s (fraction of 8 TB/s) for asum/dot/scal/gemv at "
+                      "1/2/4/8 B200",
+            "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "accum": "f32 inner folds, f64 partials and f64 gemv accumulation",
+            "data": "synthetic (seeded counter-based generator, device-filled)",
+            "config": {"workload": "step = scal+asum fp32 n=2^28 (configs[2]) + dot fp32 "
+                                   "n=2^26 (configs[1]) + gemv 8192x8192 a=1.5 b=0.5 "
+                                   "(configs[3]), per rank",
+                       "global_batch": world, "parallelism": f"shard{world} (weak)",
+                       "l2": "no flush: every operand >= 256 MiB > 126 MB L2",
+                       "frac_of_8TBs": round(value / world / NOMINAL_HBM, 4)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(dom_gbs / peak, 4),
+                         "traffic": traffic.get(dom), "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": ob[dom]},
+            "per_op": per_op,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": sampler.summary(t_wall0, max(t_wall1, t_wall2)) if sampler else None,
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_budget)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
+            max_over_ranks, barrier, step_bytes):
+    """Same metric, end to end: every step copies its inputs from pinned host memory,
+    runs the step through the public API and reads every result back to the host."""
+    steps = max(1, min(args.steps, args.e2e_steps))
+
+    def host(n, tid, i0, lo, hi):
+        t = torch.empty(n, dtype=torch.float32).pin_memory()
+        gen.fill_host(t.numpy(), 0, tid, i0, gen.DIST_UNIFORM, lo, hi)
+        return t
+
+    h_x = host(N_VEC, gen.TID_X, rank * N_VEC, -1.0, 1.0)
+    h_dx = host(N_DOT, gen.TID_X, rank * N_DOT, 0.0, 1.0)
+    h_dy = host(N_DOT, gen.TID_Y, rank * N_DOT, 0.0, 2.0)
+    h_A = host(GEMV_M * GEMV_N, gen.TID_A, rank * GEMV_M * GEMV_N, 0.0, 3.0)
+    h_gx = host(GEMV_N, gen.TID_X, 0, 0.0, 1.0)
+    h_gy = host(GEMV_M, gen.TID_Y, rank * GEMV_M, 0.0, 2.0)
+    h_yv = torch.empty(N_VEC, dtype=torch.float32).pin_memory()
+    h_res = torch.empty(2, dtype=torch.float32).pin_memory()
+    h_g = torch.empty(GEMV_M * world, dtype=torch.float32).pin_memory()
+    d = {k: torch.empty(v.numel(), dtype=torch.float32, device=dev)
+         for k, v in (("x", h_x), ("dx", h_dx), ("dy", h_dy), ("A", h_A), ("gx", h_gx),
+                      ("gy", h_gy))}
+    d_yv = torch.empty(N_VEC, dtype=torch.float32, device=dev)
+    d_res = torch.empty(2, dtype=torch.float32, device=dev)
+    d_g = torch.empty(GEMV_M, dtype=torch.float32, device=dev)
+    d_gf = torch.empty(GEMV_M * world, dtype=torch.float32, device=dev)
+    ws_a, ws_d = lift.Workspace(N_VEC, dev), lift.Workspace(N_DOT, dev)
+    h2d = sum(v.numel() * 4 for v in (h_x, h_dx, h_dy, h_A, h_gx, h_gy))
+    d2h = (N_VEC + 2 + GEMV_M * world) * 4
+
+    def e2e_step():
+        for k, h in (("x", h_x), ("dx", h_dx), ("dy", h_dy), ("A", h_A), ("gx", h_gx),
+                     ("gy", h_gy)):
+            d[k].copy_(h, non_blocking=True)
+        lift.scal(ALPHA_SCAL, d["x"], out=d_yv)
+        A = d["A"].view(GEMV_M, GEMV_N)
+        if world == 1:
+            lift.asum(d["x"], out=d_res[0:1], ws=ws_a)
+            lift.dot(d["dx"], d["dy"], out=d_res[1:2], ws=ws_d)
+            lift.gemv(A, d["gx"], d["gy"], ALPHA, BETA, out=d_gf)
+        else:
+            ldist.sharded_asum(d["x"], group, out=d_res[0:1], ws=ws_a)
+            ldist.sharded_dot(d["dx"], d["dy"], group, out=d_res[1:2], ws=ws_d)
+            ldist.sharded_gemv(A, d["gx"], d["gy"], ALPHA, BETA, GEMV_M * world, group,
+                               out_full=d_gf, out_slice=d_g)
+        h_yv.copy_(d_yv, non_blocking=True)
+        h_res.copy_(d_res, non_blocking=True)
+        h_g.copy_(d_gf, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        e2e_step()
+    e.record(stream)
+    barrier()
+    ms = max_over_ranks(s.elapsed_time(e)) / steps
+    return {"value": round(step_bytes * world / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
+            "steps": steps}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="lift", choices=["lift", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "lift":
+        print("note: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lift(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,132 @@
+/* lift.h — C ABI of liblift.so: the B200 (sm_100a) hot path of Steuwer, Fensch &
+ * Dubach, "Patterns and Rewrite Rules for Systematic Code Generation"
+ * (arXiv 1502.02389; /root/reference/PAPER.md cited as P:<line>).
+ *
+ * The four BLAS compositions of the paper's Fig. 8:
+ *     scal(a, x)          = map(mult(a), x)
+ *     asum(x)             = reduce(add, 0) o map(abs, x)
+ *     dot(x, y)           = reduce(add, 0) o map(mult) o zip(x, y)
+ *     gemv(A, x, y, a, b) = map(add) o zip(map(scal(a) o dot(x), A),
+ *                                          scal(b, y))
+ *   with abs(x) = if (x < 0) -x else x, add = +, mult = * (P:789-790),
+ *   and gemv computing "y = alpha A x + beta y".
+ *
+ * General contract (every entry point):
+ *  - Storage is fp32 (reading R1 in DESIGN.md: the paper's elements are 4 bytes,
+ *    P:1077-1080).  All array pointers are DEVICE pointers of the current CUDA
+ *    device, at least 4-byte aligned; wider alignment only enables wider loads and
+ *    never changes a result bit.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream): it validates its arguments on the host, enqueues exactly one kernel
+ *    (none for empty work) and returns.  It never synchronises, never allocates and
+ *    never touches host copies of the data.  Results are stream-ordered in device
+ *    memory; read them after your own sync.  A reduction's result is a 1-element
+ *    device array, following the paper's "primitives are arrays of length 1"
+ *     and reduce's type T[] -> T[1].
+ *  - The caller owns every buffer, including the workspace.  The library keeps no
+ *    device memory and no mutable state except a per-device cache of the SM count
+ *    and kernel occupancies (and the test hook lift_debug_set_grid_limit).
+ *  - Errors are returned synchronously and nothing is launched:
+ *      LIFT_ERR_INVALID_VALUE  n, m < 0; lda < max(1, n); p < 1; a pointer that is
+ *                              not 4-byte aligned;
+ *      LIFT_ERR_NULL_POINTER   a required pointer is NULL while the length is > 0;
+ *      LIFT_ERR_WORKSPACE      ws too small for n (see lift_workspace_bytes) or ws not
+ *                              16-B aligned;
+ *      LIFT_ERR_CUDA           the launch itself failed (cudaGetLastError).
+ *    Faults inside a kernel surface at the caller's next synchronisation.
+ *  - Determinism: every floating-point addition happens in an order that depends
+ *    only on the lengths (reading R5), so results are bit-identical run to
+ *    run, across grid sizes, SM counts and pointer alignments.
+ *  - Thread safety: all calls are reentrant.  A workspace must not be used by two
+ *    calls that can run concurrently (use one per stream).
+ */
+#ifndef LIFT_H_
+#define LIFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same object as cudaStream_t / CUstream (an opaque driver stream handle). */
+typedef struct CUstream_st* lift_stream_t;
+
+typedef enum {
+    LIFT_OK = 0,
+    LIFT_ERR_INVALID_VALUE = 1,
+    LIFT_ERR_NULL_POINTER = 2,
+    LIFT_ERR_WORKSPACE = 3,
+    LIFT_ERR_CUDA = 4
+} lift_status;
+
+/* ABI version of this header (bumped on any signature or contract change). */
+#define LIFT_ABI_VERSION 1
+int lift_abi_version(void);
+
+/* Static, NUL-terminated description of a status code. */
+const char* lift_status_string(lift_status s);
+
+/* Bytes of workspace lift_asum / lift_dot / *_partial need for length n (a multiple of
+ * 16).  The workspace holds the single-pass reduction's chunk/group partials (from its
+ * start) and its last-block-done tickets (in a tail region whose size depends only on
+ * ws_bytes).  The caller ZERO-FILLS it ONCE after allocation and then always passes the
+ * SAME ws_bytes with that buffer; every call leaves the tickets at zero again, so one
+ * buffer serves any n with lift_workspace_bytes(n) <= ws_bytes, indefinitely (unless a
+ * kernel faults, after which it must be zero-filled again). */
+size_t lift_workspace_bytes(int64_t n);
+
+/* S1 — scal: y[i] = RN_fp32(alpha * x[i]) for 0 <= i < n.
+ *   x: n floats in; y: n floats out; y == x (in place) is allowed, any other overlap
+ *   is undefined.  n == 0 launches nothing.  Bit-exact by construction. */
+lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_stream_t stream);
+
+/* R1-R4 — asum: *result = RN_fp32(sum_i |x[i]|), n == 0 -> +0.0f (z = 0,
+ *   P:794).  Single kernel, single pass (fused map+reduce, Fig. 4 (8)), with
+ *   an fp64 cross-CTA fold.  x: n floats in; result: 1 float out (device);
+ *   ws: lift_workspace_bytes(n) bytes (see above). */
+lift_status lift_asum(int64_t n, const float* x, float* result, void* ws, size_t ws_bytes,
+                      lift_stream_t stream);
+
+/* R1-R4 — dot: *result = RN_fp32(sum_i x[i]*y[i]), n == 0 -> +0.0f.
+ *   zip requires equal lengths, so one n describes both x and y. */
+lift_status lift_dot(int64_t n, const float* x, const float* y, float* result, void* ws,
+                     size_t ws_bytes, lift_stream_t stream);
+
+/* Sharding helpers: the same reductions, but the un-rounded fp64 total is written to
+ *   *partial (1 double, device) instead of an fp32 result.  Used per rank before the
+ *   cross-GPU combine (X1). */
+lift_status lift_asum_partial(int64_t n, const float* x, double* partial, void* ws,
+                              size_t ws_bytes, lift_stream_t stream);
+lift_status lift_dot_partial(int64_t n, const float* x, const float* y, double* partial,
+                             void* ws, size_t ws_bytes, lift_stream_t stream);
+
+/* X1 — combine: *result = RN_fp32(pairwise_sum(partials[0..p))), the outermost
+ *   reduce over per-rank partials in a fixed pairwise order (zero-padded to a power
+ *   of two), so every rank that calls it on the gathered partials gets the same bits.
+ *   partials: p doubles (device); result: 1 float (device); p >= 1. */
+lift_status lift_combine(int p, const double* partials, float* result, lift_stream_t stream);
+
+/* G1-G3 — gemv:
+ *   y_out[i] = RN_fp32( alpha * (sum_j A[i*lda + j] * x[j]) + beta * y[i] ),  0 <= i < m,
+ *   the dot in fp64 with exact products, the epilogue fma'd in fp64 and rounded once.
+ *   A: m x n row-major, leading dimension lda >= max(1, n) (map over rows);
+ *   x: n floats; y: m floats; y_out: m floats (y_out == y allowed).
+ *   Literal semantics (reading R11): A, x and y are always read, so NaN/Inf propagate
+ *   even when alpha or beta is 0 (no BLAS quick return).  m == 0 launches nothing;
+ *   n == 0 gives y_out = RN_fp32(beta * y). */
+lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
+                      const float* x, float beta, const float* y, float* y_out,
+                      lift_stream_t stream);
+
+/* TEST HOOK: cap the number of CTAs any subsequent launch may use (0 = no cap,
+ *   the default).  Used by the determinism tests to show results do not depend on
+ *   the grid.  Process-global; not for production use. */
+lift_status lift_debug_set_grid_limit(int max_ctas);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIFT_H_ */

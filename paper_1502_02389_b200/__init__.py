@@ -1,0 +1,185 @@
+"""paper_1502_02389_b200 — B200-native hot path of arXiv 1502.02389's BLAS compositions.
+
+Thin Python binding over liblift.so (include/lift.h): argument marshalling only.
+Every step of scal / asum / dot / gemv / combine runs in the sm_100a kernels behind
+the C ABI; PyTorch supplies device memory, streams and (in ``dist``) process groups.
+
+    scal(a, x)          = map(mult(a), x)
+    asum(x)             = reduce(add, 0) o map(abs, x)
+    dot(x, y)           = reduce(add, 0) o map(mult) o zip(x, y)
+    gemv(A, x, y, a, b) = map(add) o zip(map(scal(a) o dot(x), A), scal(b, y))
+
+Inputs must be fp32 CUDA tensors (vectors contiguous; A with unit column stride).
+Violations raise ValueError; non-OK ABI statuses raise LiftError.  There is no CPU
+fallback: a CPU tensor is an error, and a missing liblift.so fails at import.
+"""
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from ._lib import LiftError, check, lib
+
+__all__ = ["scal", "asum", "dot", "gemv", "asum_partial", "dot_partial", "combine",
+           "workspace_bytes", "Workspace", "LiftError", "set_grid_limit"]
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _vec(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be float32, got {t.dtype}")
+    if t.dim() != 1:
+        raise ValueError(f"{name} must be 1-D")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _out(out, n, dtype, device, name="out"):
+    if out is None:
+        return torch.empty(n, dtype=dtype, device=device)
+    if (not out.is_cuda or out.dtype != dtype or out.numel() != n or not out.is_contiguous()
+            or out.device != device):
+        raise ValueError(f"{name} must be a contiguous {dtype} CUDA tensor of {n} elements")
+    return out
+
+
+def workspace_bytes(n: int) -> int:
+    return int(lib.lift_workspace_bytes(int(n)))
+
+
+class Workspace:
+    """Zero-filled reduction workspace (the caller-owned buffer of lift.h).
+
+    Zero-filled once at allocation; every lift call leaves its tickets at zero, so
+    it is reusable.  Use one per stream.
+    """
+
+    def __init__(self, n: int, device):
+        self.nbytes = workspace_bytes(n)
+        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+
+_ws_lock = threading.Lock()
+_ws_cache: dict = {}
+
+
+def _workspace(n: int, device: torch.device) -> Workspace:
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    need = workspace_bytes(n)
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or ws.nbytes < need:
+            ws = Workspace(n, device)
+            _ws_cache[key] = ws
+        return ws
+
+
+def set_grid_limit(max_ctas: int) -> None:
+    """Test hook (lift_debug_set_grid_limit): cap CTAs per launch; 0 = no cap."""
+    check(lib.lift_debug_set_grid_limit(int(max_ctas)))
+
+
+def scal(alpha: float, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """y = alpha * x (lift_scal).  ``out`` may be ``x`` itself (in place)."""
+    x = _vec(x, "x")
+    y = _out(out, x.numel(), torch.float32, x.device)
+    check(lib.lift_scal(x.numel(), float(alpha), x.data_ptr(), y.data_ptr(),
+                        _stream_handle(x.device)))
+    return y
+
+
+def asum(x: torch.Tensor, out: torch.Tensor | None = None,
+         ws: Workspace | None = None) -> torch.Tensor:
+    """1-element fp32 tensor = sum |x_i| (lift_asum)."""
+    x = _vec(x, "x")
+    r = _out(out, 1, torch.float32, x.device)
+    w = ws or _workspace(x.numel(), x.device)
+    check(lib.lift_asum(x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                        _stream_handle(x.device)))
+    return r
+
+
+def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None,
+        ws: Workspace | None = None) -> torch.Tensor:
+    """1-element fp32 tensor = sum x_i*y_i (lift_dot).  zip needs equal lengths."""
+    x, y = _vec(x, "x"), _vec(y, "y")
+    if x.numel() != y.numel():
+        raise ValueError("zip-length-mismatch: dot needs equal lengths (PAPER.md P:307)")
+    if x.device != y.device:
+        raise ValueError("x and y must be on the same device")
+    r = _out(out, 1, torch.float32, x.device)
+    w = ws or _workspace(x.numel(), x.device)
+    check(lib.lift_dot(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                       _stream_handle(x.device)))
+    return r
+
+
+def asum_partial(x: torch.Tensor, out: torch.Tensor | None = None,
+                 ws: Workspace | None = None) -> torch.Tensor:
+    """1-element fp64 tensor: the un-rounded asum total (lift_asum_partial)."""
+    x = _vec(x, "x")
+    r = _out(out, 1, torch.float64, x.device)
+    w = ws or _workspace(x.numel(), x.device)
+    check(lib.lift_asum_partial(x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                                _stream_handle(x.device)))
+    return r
+
+
+def dot_partial(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None,
+                ws: Workspace | None = None) -> torch.Tensor:
+    """1-element fp64 tensor: the un-rounded dot total (lift_dot_partial)."""
+    x, y = _vec(x, "x"), _vec(y, "y")
+    if x.numel() != y.numel():
+        raise ValueError("zip-length-mismatch: dot needs equal lengths (PAPER.md P:307)")
+    r = _out(out, 1, torch.float64, x.device)
+    w = ws or _workspace(x.numel(), x.device)
+    check(lib.lift_dot_partial(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr,
+                               w.nbytes, _stream_handle(x.device)))
+    return r
+
+
+def combine(partials: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """1-element fp32 tensor = RN(pairwise sum of fp64 partials) (lift_combine)."""
+    if not (isinstance(partials, torch.Tensor) and partials.is_cuda
+            and partials.dtype == torch.float64 and partials.is_contiguous()
+            and partials.numel() >= 1):
+        raise ValueError("partials must be a non-empty contiguous float64 CUDA tensor")
+    r = _out(out, 1, torch.float32, partials.device)
+    check(lib.lift_combine(partials.numel(), partials.data_ptr(), r.data_ptr(),
+                           _stream_handle(partials.device)))
+    return r
+
+
+def gemv(A: torch.Tensor, x: torch.Tensor, y: torch.Tensor, alpha: float, beta: float,
+         out: torch.Tensor | None = None) -> torch.Tensor:
+    """y_out = alpha * A @ x + beta * y (lift_gemv), A row-major (stride(1) == 1).
+
+    ``out`` may be ``y`` (in place)."""
+    if not (isinstance(A, torch.Tensor) and A.is_cuda and A.dtype == torch.float32
+            and A.dim() == 2):
+        raise ValueError("A must be a 2-D float32 CUDA tensor")
+    m, n = A.shape
+    if m > 0 and n > 0 and A.stride(1) != 1:
+        raise ValueError("A must be row-major with unit column stride")
+    lda = A.stride(0) if (m > 1 and n > 0) else max(1, n)
+    x, y = _vec(x, "x"), _vec(y, "y")
+    if x.numel() != n or y.numel() != m:
+        raise ValueError(f"dimension-mismatch: A is {m}x{n}, x has {x.numel()}, "
+                         f"y has {y.numel()}")
+    yo = _out(out, m, torch.float32, A.device)
+    check(lib.lift_gemv(m, n, float(alpha), A.data_ptr(), lda, x.data_ptr(), float(beta),
+                        y.data_ptr(), yo.data_ptr(), _stream_handle(A.device)))
+    return yo

@@ -1,0 +1,65 @@
+"""ctypes loader for liblift.so — the C ABI declared in include/lift.h.
+
+Loading fails LOUDLY: there is no CPU or PyTorch fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+# LIFT_LIB may point at an alternative build of the same ABI (A/B tuning runs only).
+LIB_PATH = os.environ.get("LIFT_LIB") or os.path.join(_HERE, "liblift.so")
+
+# Every symbol include/lift.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "lift_abi_version", "lift_status_string", "lift_workspace_bytes", "lift_scal",
+    "lift_asum", "lift_dot", "lift_asum_partial", "lift_dot_partial", "lift_combine",
+    "lift_gemv", "lift_debug_set_grid_limit",
+)
+
+LIFT_OK = 0
+ABI_VERSION = 1
+
+_i64, _f32, _vp, _sz, _int = (ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t,
+                              ctypes.c_int)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"liblift.so not found at {LIB_PATH}: the CUDA extension is required (no CPU "
+            "fallback). Build it with `python __graft_entry__.py`.")
+    L = ctypes.CDLL(LIB_PATH)
+    sig = {
+        "lift_abi_version": ([], _int),
+        "lift_status_string": ([_int], ctypes.c_char_p),
+        "lift_workspace_bytes": ([_i64], _sz),
+        "lift_scal": ([_i64, _f32, _vp, _vp, _vp], _int),
+        "lift_asum": ([_i64, _vp, _vp, _vp, _sz, _vp], _int),
+        "lift_dot": ([_i64, _vp, _vp, _vp, _vp, _sz, _vp], _int),
+        "lift_asum_partial": ([_i64, _vp, _vp, _vp, _sz, _vp], _int),
+        "lift_dot_partial": ([_i64, _vp, _vp, _vp, _vp, _sz, _vp], _int),
+        "lift_combine": ([_int, _vp, _vp, _vp], _int),
+        "lift_gemv": ([_i64, _i64, _f32, _vp, _i64, _vp, _f32, _vp, _vp, _vp], _int),
+        "lift_debug_set_grid_limit": ([_int], _int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.lift_abi_version() != ABI_VERSION:
+        raise ImportError(f"liblift.so ABI {L.lift_abi_version()} != {ABI_VERSION}")
+    return L
+
+
+lib = _load()
+
+
+class LiftError(RuntimeError):
+    pass
+
+
+def check(status: int) -> None:
+    if status != LIFT_OK:
+        raise LiftError(lib.lift_status_string(status).decode())

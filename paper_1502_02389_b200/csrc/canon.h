@@ -1,0 +1,22 @@
+// canon.h — the canonical decomposition constants of the lift kernels.
+//
+// These fix the ORDER of every floating-point addition (reading R5),
+// so they are part of the numerical contract: changing one changes result bits
+// (never correctness).  lift_workspace_bytes() is derived from them.
+#pragma once
+
+namespace lift {
+
+// asum / dot (reduce.cuh)
+constexpr int RED_T = 256;                        // lanes per chunk (= threads per CTA)
+constexpr int RED_V = 8;                          // floats per vector slot (asVector^8)
+constexpr int RED_K = 16;                         // vectors per lane per chunk
+constexpr long long RED_C = (long long)RED_T * RED_V * RED_K;  // 32768 elements per chunk
+constexpr int RED_G = 64;                         // chunks per group (level-1 fold)
+
+// gemv (gemv.cuh)
+constexpr int GEMV_T = 256;       // threads per CTA (8 warps)
+constexpr int GEMV_V = 8;         // floats per vector slot along a row
+constexpr int GEMV_PMAX = 16384;  // max x-panel columns staged in shared memory
+
+}  // namespace lift

@@ -1,0 +1,123 @@
+// common.cuh — sm_100a building blocks shared by the lift kernels.
+//
+// The paper's low-level OpenCL patterns (Table 2) become
+// these B200 mechanisms:
+//   asVector^8 / vect^8  -> 256-bit LDG/STG (LDG.E.ENL2.256,
+//                                                  sm_100-only; 8 fp32 per lane)
+//   toLocal                   -> shared memory, filled by the TMA
+//                                                  bulk-copy engine (cp.async.bulk)
+//   iterate^k(split-2 reduce) in local memory    -> __shfl_xor butterfly
+//   reduce-seq                -> a per-thread register fold
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lift {
+
+struct f8 {
+    float v[8];
+};
+
+// 256-bit read-only streaming load (no L1 allocation): one asVector^8 element.
+__device__ __forceinline__ f8 ld_nc_v8(const float* p) {
+    f8 r;
+    asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+          "=f"(r.v[6]), "=f"(r.v[7])
+        : "l"(p));
+    return r;
+}
+
+// Coherent (non-.nc) 256-bit load: used when the input may alias the output.
+__device__ __forceinline__ f8 ld_v8(const float* p) {
+    f8 r;
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+
+__device__ __forceinline__ void st_v8(float* p, const f8& r) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                 "f"(r.v[0]), "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]),
+                 "f"(r.v[6]), "f"(r.v[7])
+                 : "memory");
+}
+
+// Load one 8-float slot with the widest access the alignment class allows.
+// LW = 8: one 256-bit load; LW = 4: two 128-bit loads; LW = 1: eight scalar loads.
+// All three return the same values, so the arithmetic order never depends on LW.
+template <int LW>
+__device__ __forceinline__ f8 ld_slot(const float* p) {
+    if constexpr (LW == 8) {
+        return ld_nc_v8(p);
+    } else if constexpr (LW == 4) {
+        f8 r;
+        float4 a = __ldg(reinterpret_cast<const float4*>(p));
+        float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        r.v[0] = a.x; r.v[1] = a.y; r.v[2] = a.z; r.v[3] = a.w;
+        r.v[4] = b.x; r.v[5] = b.y; r.v[6] = b.z; r.v[7] = b.w;
+        return r;
+    } else {
+        f8 r;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r.v[e] = __ldg(p + e);
+        return r;
+    }
+}
+
+// Fixed pairwise fold of 8 fp64 values: ((v0+v1)+(v2+v3))+((v4+v5)+(v6+v7)).
+__device__ __forceinline__ double pairwise8(const double* v) {
+    return __dadd_rn(__dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])),
+                     __dadd_rn(__dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])));
+}
+
+// Warp butterfly with xor distances 1,2,4,8,16: a pairwise tree over lanes in
+// ascending adjacent pairs (IEEE addition is commutative, so lanes i and i^d get
+// bit-identical sums).  Every lane ends with the warp total.
+__device__ __forceinline__ double warp_pairwise(double v) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, d));
+    return v;
+}
+
+// ---- mbarrier + TMA bulk copy (cp.async.bulk -> SASS UBLKCP) -------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+}  // namespace lift

@@ -1,0 +1,202 @@
+// gemv.cuh — G1..G3: y_out = alpha * A x + beta * y.
+//
+//   gemv(A, x, y, a, b):  z = map(scal(a) o dot(x), A)
+//                         map(add) o zip(z, scal(b, y))
+//
+// A is row-major with leading dimension lda (map(..., A) maps over rows, P:815;
+// DESIGN.md reading R8).  "The dot-product from gemv might be implemented in a
+// totally different way from the stand-alone dot-product" — and it is:
+//
+//  G1 toLocal(x): x is staged ONCE per CTA (per column panel of up to
+//     GEMV_PMAX columns) by the TMA bulk-copy engine (cp.async.bulk -> UBLKCP, an
+//     mbarrier tracks the bytes), then widened to fp64 into a slot-major shared
+//     layout xs[e][q] = x[8q + e], so the per-lane reads below are conflict-free
+//     LDS.64.  x is reused by every row the CTA processes.
+//  G2 per-row dot, exact products, fp64 accumulation: lane l of a warp owns the
+//     8-float vectors l, l+32, l+64, ... of a row (reorder-stride, s = 32, coalesced
+//     LDG.256); 8 fp64 accumulators per row and lane fold acc_e = fma(A_ij, x_j,
+//     acc_e) in ascending vector order (A_ij * x_j is exact in fp64, so each step
+//     rounds once).  Lane value = pairwise fold of its 8 accumulators, then the warp
+//     butterfly.  A warp carries GEMV_R rows at once so each x slot read from shared
+//     memory feeds GEMV_R rows.
+//  G3 fused epilogue (rule 5f map-map fusion): y_out_i = fp32(fma(alpha, d_i,
+//     beta * y_i)) in fp64, rounded once to fp32 (reading R10).
+//     y_out may alias y: each element is read then written by the same lane.
+//
+// The order of every addition is a function of n only (not of m, the grid, the
+// row-to-warp assignment or the panel count, since panels are multiples of 256
+// columns), so a row's result is bit-identical however the rows are sharded.
+#pragma once
+#include "common.cuh"
+#include "canon.h"
+
+namespace lift {
+
+struct GemvArgs {
+    int64_t m, n, lda;
+    float alpha, beta;
+    const float* A;
+    const float* x;
+    const float* y;
+    float* y_out;
+    int P;          // panel columns (multiple of 256, <= GEMV_PMAX)
+    int xs_stride;  // doubles per slot row of xs (= P/8 + 1, padding breaks bank conflicts)
+};
+
+__host__ __device__ constexpr size_t gemv_smem_bytes(int P) {
+    return 16 /*mbarrier*/ + (size_t)P * 4 /*fp32 stage*/ + (size_t)8 * (P / 8 + 1) * 8 /*fp64*/;
+}
+
+// Stage x[c0, c0+pc) into xs (fp64, slot-major).  Called by the whole CTA.
+__device__ __forceinline__ void gemv_stage_x(const GemvArgs& a, int64_t c0, int pc,
+                                             uint64_t* bar, float* xstage, double* xs,
+                                             uint32_t& phase) {
+    const int t = threadIdx.x;
+    const float* src = a.x + c0;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    const int nbulk = aligned ? (pc & ~3) : 0;  // elements moved by the TMA bulk copy
+    if (t == 0 && nbulk > 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(bar, (uint32_t)nbulk * 4u);
+        bulk_g2s(xstage, src, (uint32_t)nbulk * 4u, bar);
+    }
+    for (int j = nbulk + t; j < pc; j += GEMV_T) xstage[j] = __ldg(src + j);
+    __syncthreads();
+    if (nbulk > 0) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+    }
+    const int pq = (pc + 7) & ~7;
+    for (int j = t; j < pq; j += GEMV_T)
+        xs[(j & 7) * a.xs_stride + (j >> 3)] = (j < pc) ? (double)xstage[j] : 0.0;
+    __syncthreads();
+}
+
+// Fold panel columns [c0, c0+pc) of rows `rows[0..R)` into acc (lane-owned vectors).
+template <int R, int U, int LW>
+__device__ __forceinline__ void gemv_panel(const GemvArgs& a, const int64_t* rows, int64_t c0,
+                                           int pc, const double* xs, double (&acc)[R][8]) {
+    const int lane = threadIdx.x & 31;
+    const int kfull = pc / 256;  // k-steps where all 32 lanes hold a full vector
+    const float* rowp[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rowp[r] = a.A + rows[r] * a.lda + c0;
+
+    int k = 0;
+    for (; k + U <= kfull; k += U) {
+        f8 av[U][R];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                av[u][r] = ld_slot<LW>(rowp[r] + 8 * (lane + 32 * (k + u)));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = lane + 32 * (k + u);
+            double xv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) xv[e] = xs[e * a.xs_stride + q];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    acc[r][e] = __fma_rn((double)av[u][r].v[e], xv[e], acc[r][e]);
+        }
+    }
+    for (; k < kfull; ++k) {
+        const int q = lane + 32 * k;
+        f8 av[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) av[r] = ld_slot<LW>(rowp[r] + 8 * q);
+        double xv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[e] = xs[e * a.xs_stride + q];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[r][e] = __fma_rn((double)av[r].v[e], xv[e], acc[r][e]);
+    }
+    if (kfull * 256 < pc) {  // ragged last k-step: same order, columns >= pc skipped
+        const int q = lane + 32 * kfull;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int j = 8 * q + e;
+            if (j < pc) {
+                const double xj = xs[e * a.xs_stride + q];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    acc[r][e] = __fma_rn((double)__ldg(rowp[r] + j), xj, acc[r][e]);
+            }
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void gemv_epilogue(const GemvArgs& a, const int64_t* rows,
+                                              int nvalid, double (&acc)[R][8]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const double d = warp_pairwise(pairwise8(acc[r]));
+        if (lane == r && r < nvalid) {
+            const int64_t i = rows[r];
+            const double w = __dmul_rn((double)a.beta, (double)a.y[i]);  // scal(b, y): exact
+            a.y_out[i] = __double2float_rn(__fma_rn((double)a.alpha, d, w));
+        }
+    }
+}
+
+// MULTI = false: n <= P, x staged once, rows assigned per warp (no CTA syncs after
+// staging).  MULTI = true: n > P, rows assigned per CTA block, x re-staged per panel.
+template <int R, int U, int LW, bool MULTI>
+__global__ void __launch_bounds__(GEMV_T) gemv_kernel(GemvArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    float* xstage = reinterpret_cast<float*>(smem + 16);
+    double* xs = reinterpret_cast<double*>(smem + 16 + (size_t)a.P * 4);
+    const int warp = threadIdx.x >> 5;
+    uint32_t phase = 0;
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+
+    if constexpr (!MULTI) {
+        gemv_stage_x(a, 0, (int)a.n, bar, xstage, xs, phase);
+        const int64_t total_warps = (int64_t)gridDim.x * (GEMV_T / 32);
+        for (int64_t r0 = ((int64_t)blockIdx.x * (GEMV_T / 32) + warp) * R; r0 < a.m;
+             r0 += total_warps * R) {
+            int64_t rows[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) rows[r] = min(r0 + r, a.m - 1);
+            double acc[R][8];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
+            gemv_panel<R, U, LW>(a, rows, 0, (int)a.n, xs, acc);
+            gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
+        }
+    } else {
+        const int64_t rows_per_block = (int64_t)(GEMV_T / 32) * R;
+        for (int64_t b0 = (int64_t)blockIdx.x * rows_per_block; b0 < a.m;
+             b0 += (int64_t)gridDim.x * rows_per_block) {
+            const int64_t r0 = b0 + (int64_t)warp * R;
+            int64_t rows[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) rows[r] = min(r0 + r, a.m - 1);
+            double acc[R][8];
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
+            for (int64_t c0 = 0; c0 < a.n; c0 += a.P) {
+                const int pc = (int)min((int64_t)a.P, a.n - c0);
+                gemv_stage_x(a, c0, pc, bar, xstage, xs, phase);
+                gemv_panel<R, U, LW>(a, rows, c0, pc, xs, acc);
+                __syncthreads();  // all warps done with xs before the next panel
+            }
+            if (r0 < a.m) gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
+        }
+    }
+}
+
+}  // namespace lift

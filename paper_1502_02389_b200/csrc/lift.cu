@@ -1,0 +1,343 @@
+// lift.cu — the C ABI of liblift.so (include/lift.h): argument checks, launch
+// configuration and the cross-rank combine kernel.  Every step of the hot path runs
+// in the kernels of scal.cuh, reduce.cuh and gemv.cuh; this file only validates and
+// launches (no host arithmetic on the data, no CPU fallback).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+
+#include "../../include/lift.h"
+#include "canon.h"
+#include "common.cuh"
+#include "gemv.cuh"
+#include "reduce.cuh"
+#include "scal.cuh"
+
+#ifndef LIFT_GEMV_R
+#define LIFT_GEMV_R 2  // rows per warp
+#endif
+#ifndef LIFT_GEMV_U
+#define LIFT_GEMV_U 4  // k-steps of loads in flight per row
+#endif
+#ifndef LIFT_ASUM_B
+#define LIFT_ASUM_B 8  // 256-bit loads in flight per lane (asum)
+#endif
+#ifndef LIFT_DOT_B
+#define LIFT_DOT_B 4   // vector pairs in flight per lane (dot)
+#endif
+#ifndef LIFT_RED_ACC
+#define LIFT_RED_ACC double  // per-lane accumulator of asum/dot (canonical order, R13)
+#endif
+
+namespace lift {
+
+// X1: outermost reduce over p per-rank fp64 partials, pairwise (zero-padded to 2^k).
+__global__ void combine_kernel(int p, const double* __restrict__ partials, float* result) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t p2 = 1;
+    while (p2 < p) p2 <<= 1;
+    double stk[40];
+    int top = 0;
+    for (int64_t i = 0; i < p2; ++i) {
+        double w = (i < p) ? partials[i] : 0.0;
+        for (int64_t cnt = i; cnt & 1; cnt >>= 1) w = __dadd_rn(stk[--top], w);
+        stk[top++] = w;
+    }
+    *result = __double2float_rn(stk[0]);
+}
+
+namespace {
+
+std::atomic<int> g_grid_limit{0};
+
+struct DevInfo {
+    int sms = 0;
+};
+DevInfo g_dev[64];
+std::mutex g_mu;
+
+struct OccEntry {
+    const void* fn;
+    int dev;
+    size_t smem;
+    int blocks;
+};
+OccEntry g_occ[256];
+int g_nocc = 0;
+
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+int sm_count(int dev) {
+    if (dev < 0 || dev >= 64) return 148;
+    if (g_dev[dev].sms == 0) {
+        int s = 0;
+        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+        g_dev[dev].sms = s > 0 ? s : 148;
+    }
+    return g_dev[dev].sms;
+}
+
+// Resident CTAs per SM for `fn` (cached).  Also raises the dynamic smem limit.
+int occupancy(const void* fn, int threads, size_t smem) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (int i = 0; i < g_nocc; ++i)
+        if (g_occ[i].fn == fn && g_occ[i].dev == dev && g_occ[i].smem == smem)
+            return g_occ[i].blocks;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess ||
+        b < 1)
+        b = 1;
+    if (g_nocc < 256) g_occ[g_nocc++] = OccEntry{fn, dev, smem, b};
+    return b;
+}
+
+int64_t grid_for(int64_t work_ctas, const void* fn, int threads, size_t smem) {
+    const int dev = current_device();
+    int64_t g = (int64_t)sm_count(dev) * occupancy(fn, threads, smem);
+    if (work_ctas < g) g = work_ctas;
+    const int lim = g_grid_limit.load();
+    if (lim > 0 && g > lim) g = lim;
+    return g < 1 ? 1 : g;
+}
+
+inline bool misaligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3) != 0; }
+inline int align_class(uintptr_t a) { return (a & 31) == 0 ? 8 : ((a & 15) == 0 ? 4 : 1); }
+
+lift_status launched() {
+    return cudaGetLastError() == cudaSuccess ? LIFT_OK : LIFT_ERR_CUDA;
+}
+
+// Workspace layout for a buffer of W bytes (W floored to 16):
+//   [chunk partials f64 x nc][group partials f64 x ng] ... [tickets u32, last R(W) bytes]
+// The ticket region depends on W ONLY, so every call made on the same buffer (with the
+// same ws_bytes) agrees where the tickets live, and no call's partials ever overlap any
+// call's tickets — the tickets stay zero across calls of different n (the contract's
+// "zero-fill once").  R(W) holds W/512 + 2 tickets, enough for the largest n that fits.
+inline size_t ticket_region(size_t wf) { return ((wf / 512 + 2) * 4 + 15) & ~(size_t)15; }
+
+struct WsLayout {
+    int64_t nc, ng;
+    size_t partial_bytes;
+};
+WsLayout ws_layout(int64_t n) {
+    WsLayout L;
+    L.nc = (n + RED_C - 1) / RED_C;
+    L.ng = (L.nc + RED_G - 1) / RED_G;
+    L.partial_bytes = 8 * (size_t)(L.nc + L.ng);
+    return L;
+}
+bool ws_fits(const WsLayout& L, size_t wbytes) {
+    const size_t wf = wbytes & ~(size_t)15;
+    const size_t r = ticket_region(wf);
+    return wf >= r && wf - r >= L.partial_bytes && (size_t)(L.ng + 1) * 4 <= r;
+}
+size_t ws_bytes_for(int64_t n) {
+    const WsLayout L = ws_layout(n);
+    size_t w = (L.partial_bytes + L.partial_bytes / 127 + 32 + 15) & ~(size_t)15;
+    while (!ws_fits(L, w)) w += 16;
+    return w;
+}
+
+template <class Op, int B>
+lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out32, double* out64,
+                          void* ws, size_t ws_bytes, cudaStream_t stream) {
+    if (n < 0) return LIFT_ERR_INVALID_VALUE;
+    if (!out32 && !out64) return LIFT_ERR_NULL_POINTER;
+    if (n > 0 && (!x || (Op::kTwoInputs && !y) || !ws)) return LIFT_ERR_NULL_POINTER;
+    if (misaligned4(x) || (Op::kTwoInputs && misaligned4(y)) || misaligned4(out32) ||
+        (reinterpret_cast<uintptr_t>(out64) & 7))
+        return LIFT_ERR_INVALID_VALUE;
+    if (n == 0) {  // reduce over an empty array yields z = +0
+        if (out32 && cudaMemsetAsync(out32, 0, sizeof(float), stream) != cudaSuccess)
+            return LIFT_ERR_CUDA;
+        if (out64 && cudaMemsetAsync(out64, 0, sizeof(double), stream) != cudaSuccess)
+            return LIFT_ERR_CUDA;
+        return LIFT_OK;
+    }
+    const WsLayout L = ws_layout(n);
+    if (!ws_fits(L, ws_bytes) || (reinterpret_cast<uintptr_t>(ws) & 15)) return LIFT_ERR_WORKSPACE;
+    const size_t wf = ws_bytes & ~(size_t)15;
+
+    ReduceArgs a;
+    a.n = n;
+    a.x = x;
+    a.y = y;
+    a.nc = L.nc;
+    a.ng = L.ng;
+    a.tick = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + wf - ticket_region(wf));
+    a.chunk_part = reinterpret_cast<double*>(ws);
+    a.group_part = a.chunk_part + L.nc;
+    a.out_f32 = out32;
+    a.out_f64 = out64;
+
+    uintptr_t al = reinterpret_cast<uintptr_t>(x);
+    if (Op::kTwoInputs) al |= reinterpret_cast<uintptr_t>(y);
+    const int lw = align_class(al);
+    const void* fn = lw == 8 ? (const void*)reduce_kernel<Op, 8, B>
+                   : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
+                             : (const void*)reduce_kernel<Op, 1, B>;
+    const int64_t grid = grid_for(L.nc, fn, RED_T, 0);
+    if (lw == 8) reduce_kernel<Op, 8, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
+    else if (lw == 4) reduce_kernel<Op, 4, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
+    else reduce_kernel<Op, 1, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
+    return launched();
+}
+
+template <int LW, bool ALIAS>
+void scal_go(int64_t grid, int64_t nslots, int head, int tail, float alpha, const float* x,
+             float* y, cudaStream_t s) {
+    scal_kernel<LW, ALIAS><<<(unsigned)grid, SCAL_T, 0, s>>>(nslots, head, tail, alpha, x, y);
+}
+
+template <int LW>
+const void* scal_fn(bool alias) {
+    return alias ? (const void*)scal_kernel<LW, true> : (const void*)scal_kernel<LW, false>;
+}
+
+template <int LW, bool MULTI>
+lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
+    constexpr int R = LIFT_GEMV_R, U = LIFT_GEMV_U;
+    const size_t smem = gemv_smem_bytes(a.P);
+    const void* fn = (const void*)gemv_kernel<R, U, LW, MULTI>;
+    const int64_t rows_per_cta = (int64_t)(GEMV_T / 32) * R;
+    const int64_t work = (a.m + rows_per_cta - 1) / rows_per_cta;
+    const int64_t grid = grid_for(work, fn, GEMV_T, smem);
+    gemv_kernel<R, U, LW, MULTI><<<(unsigned)grid, GEMV_T, smem, s>>>(a);
+    return launched();
+}
+
+}  // namespace
+}  // namespace lift
+
+using namespace lift;
+
+extern "C" {
+
+int lift_abi_version(void) { return LIFT_ABI_VERSION; }
+
+const char* lift_status_string(lift_status s) {
+    switch (s) {
+        case LIFT_OK: return "LIFT_OK";
+        case LIFT_ERR_INVALID_VALUE: return "LIFT_ERR_INVALID_VALUE: bad length, stride or alignment";
+        case LIFT_ERR_NULL_POINTER: return "LIFT_ERR_NULL_POINTER: required pointer is NULL";
+        case LIFT_ERR_WORKSPACE: return "LIFT_ERR_WORKSPACE: workspace too small or misaligned";
+        case LIFT_ERR_CUDA: return "LIFT_ERR_CUDA: kernel launch failed";
+    }
+    return "LIFT_ERR_UNKNOWN";
+}
+
+size_t lift_workspace_bytes(int64_t n) { return ws_bytes_for(n < 0 ? 0 : n); }
+
+lift_status lift_debug_set_grid_limit(int max_ctas) {
+    if (max_ctas < 0) return LIFT_ERR_INVALID_VALUE;
+    g_grid_limit.store(max_ctas);
+    return LIFT_OK;
+}
+
+lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_stream_t stream) {
+    if (n < 0) return LIFT_ERR_INVALID_VALUE;
+    if (n == 0) return LIFT_OK;
+    if (!x || !y) return LIFT_ERR_NULL_POINTER;
+    if (misaligned4(x) || misaligned4(y)) return LIFT_ERR_INVALID_VALUE;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const uintptr_t ax = reinterpret_cast<uintptr_t>(x), ay = reinterpret_cast<uintptr_t>(y);
+    const int lw = align_class(ax - ay);      // relative phase of x and y
+    const uintptr_t boundary = (uintptr_t)lw * 4;
+    int64_t head = (int64_t)(((boundary - (ax % boundary)) % boundary) / 4);
+    if (head > n) head = n;
+    const int64_t body = n - head;
+    const int64_t nslots = body / 8;
+    const int tail = (int)(body % 8);
+    const bool alias = (x == y);
+    const void* fn = lw == 8 ? scal_fn<8>(alias) : lw == 4 ? scal_fn<4>(alias) : scal_fn<1>(alias);
+    const int64_t tile = (int64_t)SCAL_T * SCAL_U;
+    const int64_t grid = grid_for((nslots + tile - 1) / tile, fn, SCAL_T, 0);
+    if (lw == 8) alias ? scal_go<8, true>(grid, nslots, (int)head, tail, alpha, x, y, s)
+                       : scal_go<8, false>(grid, nslots, (int)head, tail, alpha, x, y, s);
+    else if (lw == 4) alias ? scal_go<4, true>(grid, nslots, (int)head, tail, alpha, x, y, s)
+                            : scal_go<4, false>(grid, nslots, (int)head, tail, alpha, x, y, s);
+    else alias ? scal_go<1, true>(grid, nslots, (int)head, tail, alpha, x, y, s)
+               : scal_go<1, false>(grid, nslots, (int)head, tail, alpha, x, y, s);
+    return launched();
+}
+
+lift_status lift_asum(int64_t n, const float* x, float* result, void* ws, size_t ws_bytes,
+                      lift_stream_t stream) {
+    if (!result) return LIFT_ERR_NULL_POINTER;
+    return reduce_launch<AsumOp<LIFT_RED_ACC>, LIFT_ASUM_B>(n, x, nullptr, result, nullptr, ws, ws_bytes,
+                                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+lift_status lift_dot(int64_t n, const float* x, const float* y, float* result, void* ws,
+                     size_t ws_bytes, lift_stream_t stream) {
+    if (!result) return LIFT_ERR_NULL_POINTER;
+    return reduce_launch<DotOp<LIFT_RED_ACC>, LIFT_DOT_B>(n, x, y, result, nullptr, ws, ws_bytes,
+                                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+lift_status lift_asum_partial(int64_t n, const float* x, double* partial, void* ws,
+                              size_t ws_bytes, lift_stream_t stream) {
+    if (!partial) return LIFT_ERR_NULL_POINTER;
+    return reduce_launch<AsumOp<LIFT_RED_ACC>, LIFT_ASUM_B>(n, x, nullptr, nullptr, partial, ws, ws_bytes,
+                                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+lift_status lift_dot_partial(int64_t n, const float* x, const float* y, double* partial,
+                             void* ws, size_t ws_bytes, lift_stream_t stream) {
+    if (!partial) return LIFT_ERR_NULL_POINTER;
+    return reduce_launch<DotOp<LIFT_RED_ACC>, LIFT_DOT_B>(n, x, y, nullptr, partial, ws, ws_bytes,
+                                            reinterpret_cast<cudaStream_t>(stream));
+}
+
+lift_status lift_combine(int p, const double* partials, float* result, lift_stream_t stream) {
+    if (p < 1) return LIFT_ERR_INVALID_VALUE;
+    if (!partials || !result) return LIFT_ERR_NULL_POINTER;
+    if ((reinterpret_cast<uintptr_t>(partials) & 7) || misaligned4(result))
+        return LIFT_ERR_INVALID_VALUE;
+    combine_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p, partials, result);
+    return launched();
+}
+
+lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
+                      const float* x, float beta, const float* y, float* y_out,
+                      lift_stream_t stream) {
+    if (m < 0 || n < 0) return LIFT_ERR_INVALID_VALUE;
+    if (lda < (n > 1 ? n : 1)) return LIFT_ERR_INVALID_VALUE;
+    if (m == 0) return LIFT_OK;
+    if (!y || !y_out || (n > 0 && (!A || !x))) return LIFT_ERR_NULL_POINTER;
+    if (misaligned4(A) || misaligned4(x) || misaligned4(y) || misaligned4(y_out))
+        return LIFT_ERR_INVALID_VALUE;
+    GemvArgs a;
+    a.m = m;
+    a.n = n;
+    a.lda = lda;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.A = A;
+    a.x = x;
+    a.y = y;
+    a.y_out = y_out;
+    const bool multi = n > GEMV_PMAX;
+    a.P = multi ? GEMV_PMAX : (int)(((n > 0 ? n : 1) + 255) / 256 * 256);
+    a.xs_stride = a.P / 8 + 1;
+    const uintptr_t aa = reinterpret_cast<uintptr_t>(A);
+    const int lw = ((aa & 31) == 0 && lda % 8 == 0) ? 8 : ((aa & 15) == 0 && lda % 4 == 0) ? 4 : 1;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (multi) {
+        return lw == 8 ? gemv_go<8, true>(a, s) : lw == 4 ? gemv_go<4, true>(a, s)
+                                                          : gemv_go<1, true>(a, s);
+    }
+    return lw == 8 ? gemv_go<8, false>(a, s) : lw == 4 ? gemv_go<4, false>(a, s)
+                                                       : gemv_go<1, false>(a, s);
+}
+
+}  // extern "C"

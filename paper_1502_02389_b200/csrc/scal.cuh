@@ -1,0 +1,86 @@
+// scal.cuh — S1: y = alpha * x, the paper's scal(a, x) = map(mult(a), x)
+// (PAPER.md P:793).
+//
+// The paper lowers it as join o map-workgroup(asScalar o map-local(vect-4(mul3)) o
+// asVector-4) o split-1024 (Fig. 3b; Fig. 3c).  On B200 the
+// same structure becomes a grid-stride loop over tiles of SCAL_T x SCAL_U slots of
+// 8 floats: map-workgroup -> CTAs over tiles, map-local -> threads over slots,
+// asVector-8 -> one 256-bit LDG/STG per slot.  Unlike Fig. 3c's
+// `i < len/1024` loop (which drops the tail), any n >= 0 and any 4-byte alignment
+// are handled: a scalar head brings x to the vector alignment, a scalar tail
+// finishes the last < 8 elements; both run in CTA 0 of the same launch.
+// Every element is RN(alpha * x_i), so the result is bit-exact regardless of LW.
+#pragma once
+#include "common.cuh"
+
+namespace lift {
+
+constexpr int SCAL_T = 256;  // threads per CTA
+constexpr int SCAL_U = 4;    // 8-float slots per thread per tile (4 x 32 B in flight)
+
+template <int LW>
+__device__ __forceinline__ void st_slot(float* p, const f8& v) {
+    if constexpr (LW == 8) {
+        st_v8(p, v);
+    } else if constexpr (LW == 4) {
+        reinterpret_cast<float4*>(p)[0] = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
+        reinterpret_cast<float4*>(p)[1] = make_float4(v.v[4], v.v[5], v.v[6], v.v[7]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p[e] = v.v[e];
+    }
+}
+
+template <int LW, bool ALIAS>
+__device__ __forceinline__ f8 scal_load(const float* p) {
+    if constexpr (LW == 8 && ALIAS) return ld_v8(p);  // x == y: stay off the .nc path
+    else if constexpr (ALIAS) {
+        f8 r;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r.v[e] = p[e];
+        return r;
+    } else return ld_slot<LW>(p);
+}
+
+// head: elements [0, head) ; body: nslots slots of 8 starting at element `head` ;
+// tail: elements [head + 8*nslots, head + 8*nslots + tail).
+template <int LW, bool ALIAS>
+__global__ void __launch_bounds__(SCAL_T) scal_kernel(int64_t nslots, int head, int tail,
+                                                      float alpha, const float* x, float* y) {
+    const int t = threadIdx.x;
+    if (blockIdx.x == 0) {
+        if (t < head) y[t] = alpha * x[t];
+        const int64_t tb = head + 8 * nslots;
+        if (t >= 32 && t < 32 + tail) y[tb + (t - 32)] = alpha * x[tb + (t - 32)];
+    }
+    const float* xb = x + head;
+    float* yb = y + head;
+    constexpr int64_t TILE = (int64_t)SCAL_T * SCAL_U;
+    for (int64_t s0 = (int64_t)blockIdx.x * TILE; s0 < nslots; s0 += (int64_t)gridDim.x * TILE) {
+        if (s0 + TILE <= nslots) {
+            f8 v[SCAL_U];
+#pragma unroll
+            for (int u = 0; u < SCAL_U; ++u)
+                v[u] = scal_load<LW, ALIAS>(xb + 8 * (s0 + u * SCAL_T + t));
+#pragma unroll
+            for (int u = 0; u < SCAL_U; ++u) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[u].v[e] = __fmul_rn(alpha, v[u].v[e]);
+                st_slot<LW>(yb + 8 * (s0 + u * SCAL_T + t), v[u]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < SCAL_U; ++u) {
+                const int64_t s = s0 + u * SCAL_T + t;
+                if (s < nslots) {
+                    f8 v = scal_load<LW, ALIAS>(xb + 8 * s);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v.v[e] = __fmul_rn(alpha, v.v[e]);
+                    st_slot<LW>(yb + 8 * s, v);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace lift

@@ -1,0 +1,130 @@
+"""X1 — sharding across GPUs (one process per GPU, torch.distributed over NCCL).
+
+The paper runs on one device; sharding comes from BASELINE.json's
+north star: "Each rank reduces its shard, and one NCCL allreduce of a scalar, or a
+gather of y slices over NVLink, combines them."
+
+  scal  — contiguous shards, independent: NO collective.
+  asum, dot — each rank folds its shard to an fp64 partial (lift_*_partial); ONE
+          exchange (all-gather of p x 8 bytes) and a fixed-order pairwise combine
+          (lift_combine) give every rank the same fp32 bits.  We gather instead of
+          all-reducing so the combine order never depends on NCCL's algorithm
+          (ring / tree / NVLS); the cost is identical at 8 bytes per rank.
+  gemv  — rows are sharded, x is replicated (each rank generates or holds it), y is
+          sharded; ONE exchange: all-gather of the y_out slices.
+
+Shard boundaries for reductions are aligned to the canonical group size
+(RED_G * RED_C = 2^21 elements) when possible, so that with a power-of-two number of
+groups per rank the combined result is bit-identical to the unsharded one
+(reading R5).
+
+The collective plumbing is kept separate from the CUDA calls (``gather_partials``,
+``gather_rows``) so it can be exercised with the gloo backend on CPU; the combine
+itself always runs in liblift (``combine_fn`` is injectable only for those tests).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+GROUP_ELEMS = 64 * 32768  # RED_G * RED_C (csrc/canon.h)
+
+
+def shard_range(n: int, rank: int, world: int, align: int = GROUP_ELEMS) -> tuple[int, int]:
+    """Contiguous [start, stop) of rank `rank` in a length-n vector.
+
+    Boundaries are multiples of `align` (the last rank takes the remainder) when n is
+    large enough that every rank gets at least one aligned block; otherwise an even
+    split.  The ranges tile [0, n) exactly, in rank order."""
+    if world < 1 or not 0 <= rank < world or n < 0:
+        raise ValueError("bad shard request")
+    if align > 1 and n >= align * world:
+        blocks = -(-n // align)
+        per = blocks // world
+        extra = blocks % world
+        b0 = rank * per + min(rank, extra)
+        b1 = b0 + per + (1 if rank < extra else 0)
+        return min(n, b0 * align), min(n, b1 * align)
+    base, rem = divmod(n, world)
+    a = rank * base + min(rank, rem)
+    return a, a + base + (1 if rank < rem else 0)
+
+
+def row_range(m: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [start, stop) owned by `rank` for gemv (even split, rank order)."""
+    return shard_range(m, rank, world, align=1)
+
+
+def _world(group):
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
+def gather_partials(partial: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather one fp64 partial per rank into a rank-ordered [p] tensor."""
+    p = _world(group)
+    if p == 1:
+        return partial.reshape(1)
+    out = torch.empty(p, dtype=partial.dtype, device=partial.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, partial.reshape(1), group=group)
+    else:
+        parts = [torch.empty(1, dtype=partial.dtype, device=partial.device) for _ in range(p)]
+        dist.all_gather(parts, partial.reshape(1), group=group)
+        out.copy_(torch.cat(parts))
+    return out
+
+
+def gather_rows(y_slice: torch.Tensor, m: int, group=None, out: torch.Tensor | None = None):
+    """All-gather rank-ordered y slices (row_range split) into the full length-m y."""
+    p = _world(group)
+    if out is None:
+        out = torch.empty(m, dtype=y_slice.dtype, device=y_slice.device)
+    if p == 1:
+        out.copy_(y_slice)
+        return out
+    rank = dist.get_rank(group)
+    sizes = [row_range(m, r, p)[1] - row_range(m, r, p)[0] for r in range(p)]
+    if y_slice.numel() != sizes[rank]:
+        raise ValueError("y slice does not match row_range")
+    if len(set(sizes)) == 1 and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, y_slice, group=group)
+        return out
+    mx = max(sizes)
+    padded = torch.zeros(mx, dtype=y_slice.dtype, device=y_slice.device)
+    padded[:y_slice.numel()] = y_slice
+    parts = [torch.empty(mx, dtype=y_slice.dtype, device=y_slice.device) for _ in range(p)]
+    dist.all_gather(parts, padded, group=group)
+    out.copy_(torch.cat([parts[r][:sizes[r]] for r in range(p)]))
+    return out
+
+
+def _lift():
+    import paper_1502_02389_b200 as lift
+    return lift
+
+
+def sharded_scal(alpha: float, x_shard: torch.Tensor, out=None):
+    """scal needs no exchange: each rank scales its own shard."""
+    return _lift().scal(alpha, x_shard, out=out)
+
+
+def sharded_asum(x_shard: torch.Tensor, group=None, combine_fn=None, out=None, ws=None):
+    lift = _lift()
+    part = lift.asum_partial(x_shard, ws=ws)
+    allp = gather_partials(part, group)
+    return (combine_fn or lift.combine)(allp, out=out)
+
+
+def sharded_dot(x_shard: torch.Tensor, y_shard: torch.Tensor, group=None, combine_fn=None,
+                out=None, ws=None):
+    lift = _lift()
+    part = lift.dot_partial(x_shard, y_shard, ws=ws)
+    allp = gather_partials(part, group)
+    return (combine_fn or lift.combine)(allp, out=out)
+
+
+def sharded_gemv(A_rows: torch.Tensor, x: torch.Tensor, y_rows: torch.Tensor, alpha: float,
+                 beta: float, m: int, group=None, out_full=None, out_slice=None):
+    """Each rank computes its rows' y_out slice, then all ranks gather the full y."""
+    ys = _lift().gemv(A_rows, x, y_rows, alpha, beta, out=out_slice)
+    return gather_rows(ys, m, group, out=out_full)

@@ -1,0 +1,72 @@
+"""A/B timing of liblift builds: python scripts/ab.py lib1.so [lib2.so ...]
+
+Each library (same ABI, different compile-time tuning) runs in its own subprocess
+(LIFT_LIB=...).  Per op: median of R event-timed launches, inputs > L2 (no reuse
+between launches: operands are >= 256 MiB).  Prints one JSON line per library."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def child(reps=30):
+    import torch
+    import lift_inputs as gen
+    import paper_1502_02389_b200 as lift
+    dev = torch.device("cuda:0")
+
+    def fill(n, tid, lo, hi):
+        return gen.fill_device(torch.empty(n, dtype=torch.float32, device=dev), 0, tid, 0, 0, lo, hi)
+
+    x = fill(1 << 28, 1, -1.0, 1.0)
+    y = torch.empty(1 << 28, dtype=torch.float32, device=dev)
+    dx = fill(1 << 26, 1, 0.0, 1.0)
+    dy = fill(1 << 26, 2, 0.0, 2.0)
+    A = fill(8192 * 8192, 3, 0.0, 3.0).view(8192, 8192)
+    A2 = fill(8192 * 16384, 3, 0.0, 3.0).view(8192, 16384)
+    gx = fill(8192, 1, 0.0, 1.0)
+    gx2 = fill(16384, 1, 0.0, 1.0)
+    gy = fill(8192, 2, 0.0, 2.0)
+    go = torch.empty(8192, dtype=torch.float32, device=dev)
+    r = torch.empty(1, dtype=torch.float32, device=dev)
+    ws = lift.Workspace(1 << 28, dev)
+    ops = {
+        "scal_2p28": (lambda: lift.scal(3.0, x, out=y), 8 << 28),
+        "asum_2p28": (lambda: lift.asum(x, out=r, ws=ws), 4 << 28),
+        "dot_2p26": (lambda: lift.dot(dx, dy, out=r, ws=ws), 8 << 26),
+        "gemv_8192": (lambda: lift.gemv(A, gx, gy, 1.5, 0.5, out=go), 4 * (8192 * 8192 + 3 * 8192)),
+        "gemv_8192x16384": (lambda: lift.gemv(A2, gx2, gy, 1.5, 0.5, out=go),
+                            4 * (8192 * 16384 + 16384 + 2 * 8192)),
+        "asum_2p20": (lambda: lift.asum(x[:1 << 20], out=r, ws=ws), 4 << 20),
+    }
+    out = {}
+    for name, (fn, nbytes) in ops.items():
+        for _ in range(5):
+            fn()
+        ts = []
+        for _ in range(reps):
+            s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e))
+        ts.sort()
+        med = ts[len(ts) // 2]
+        out[name] = {"us": round(med * 1e3, 2), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1)}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    if sys.argv[1:2] == ["--child"]:
+        child()
+        sys.exit(0)
+    for lib in sys.argv[1:]:
+        env = dict(os.environ, LIFT_LIB=os.path.abspath(lib))
+        r = subprocess.run([sys.executable, __file__, "--child"], env=env, capture_output=True,
+                           text=True)
+        print(json.dumps({"lib": os.path.basename(lib)}), r.stdout.strip(), r.stderr[-2000:],
+              flush=True)

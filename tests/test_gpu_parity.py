@@ -1,0 +1,413 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * scal: bit-exact RN(alpha*x_i) at every size, alignment and aliasing;
+  * asum/dot: relative error <= 1e-5 (condition-scaled, |g-o| <= 1e-5*sum|terms|,
+    for signed dot inputs); bit-exact on integer-valued inputs, where the sum is
+    unique; bit-identical run to run and across grid sizes;
+  * gemv: per element relative error <= 1e-6 (condition-scaled for signed inputs);
+    identity matrix bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import lift_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+RED_C = 32768  # canonical chunk (csrc/canon.h)
+
+
+@pytest.fixture(scope="module")
+def lift():
+    import paper_1502_02389_b200 as m
+    m.set_grid_limit(0)
+    yield m
+    m.set_grid_limit(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def at_offset(a, off):
+    """Device copy of `a` whose data pointer is `off` floats past a 512-B boundary."""
+    buf = torch.empty(a.size + off + 8, dtype=torch.float32, device=DEV)
+    v = buf[off:off + a.size]
+    v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return v
+
+
+def bits(t):
+    return t.detach().cpu().numpy().view(np.uint32).copy()
+
+
+# ------------------------------------------------------------------ generator twin
+@pytest.mark.parametrize("dist,lo,hi", [(0, -1.0, 1.0), (0, 0.0, 3.0), (1, 0.0, 0.0)])
+def test_device_generator_matches_host(dist, lo, hi):
+    for seed, tid, i0, n in [(0, 1, 0, 1 << 20), (3, 3, (1 << 31) + 5, 100_003)]:
+        t = torch.empty(n, dtype=torch.float32, device=DEV)
+        gen.fill_device(t, seed, tid, i0, dist, lo, hi)
+        h = gen.host(n, seed, tid, i0, dist, lo, hi)
+        assert np.array_equal(bits(t), h.view(np.uint32))
+
+
+# ------------------------------------------------------------------------- scal
+SIZES_SMALL = [0, 1, 2, 3, 7, 8, 9, 15, 16, 17, 31, 255, 256, 257, 1023, 1024, 1100]
+
+
+@pytest.mark.parametrize("n", SIZES_SMALL + [8191, 8192, 8193, 100_003, 1 << 20])
+def test_scal_bit_exact(lift, n):
+    x = gen.host(n, 11, gen.TID_X, lo=-1e3, hi=1e3)
+    for alpha in (3.0, -0.7):
+        ref = oracle.scal(alpha, x).astype(np.float32)
+        got = lift.scal(alpha, dev(x)).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("ox,oy", [(0, 0), (1, 1), (3, 3), (7, 7), (1, 0), (0, 3), (2, 6), (5, 1)])
+def test_scal_alignments(lift, ox, oy):
+    n = 5003
+    x = gen.host(n, 12, gen.TID_X)
+    ref = oracle.scal(3.0, x).astype(np.float32)
+    xd = at_offset(x, ox)
+    y = torch.empty(n + oy + 8, dtype=torch.float32, device=DEV)[oy:oy + n]
+    lift.scal(3.0, xd, out=y)
+    assert np.array_equal(bits(y), ref.view(np.uint32))
+
+
+def test_scal_in_place(lift):
+    x = gen.host(77_777, 13, gen.TID_X)
+    ref = oracle.scal(-2.5, x).astype(np.float32)
+    for off in (0, 3):
+        xd = at_offset(x, off)
+        lift.scal(-2.5, xd, out=xd)
+        assert np.array_equal(bits(xd), ref.view(np.uint32))
+
+
+def test_scal_special_values(lift):
+    x = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-45, 3e38, -1.0], np.float32)
+    got = lift.scal(3.0, dev(x)).cpu().numpy()
+    ref = oracle.scal(3.0, x).astype(np.float32)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    m = ~np.isnan(ref)
+    assert np.array_equal(got[m].view(np.uint32), ref[m].view(np.uint32))  # no FTZ (1e-45*3)
+
+
+# ------------------------------------------------------------------- asum / dot
+RED_SIZES = [1, 2, 7, 8, 9, 255, 256, 257, 4096, RED_C - 1, RED_C, RED_C + 1,
+             3 * RED_C + 17, 100_003, 64 * RED_C - 5, 64 * RED_C + 7, (1 << 22) + 3]
+
+
+@pytest.mark.parametrize("n", RED_SIZES)
+def test_asum_dot_tolerance(lift, n):
+    x = gen.host(n, 21, gen.TID_X)
+    y = gen.host(n, 21, gen.TID_Y, lo=0.0, hi=2.0)
+    a = float(lift.asum(dev(x)).item())
+    ao = oracle.asum(x)
+    assert abs(a - ao) <= 1e-5 * ao
+    xp = gen.host(n, 21, gen.TID_X, lo=0.0, hi=1.0)
+    d = float(lift.dot(dev(xp), dev(y)).item())
+    do = oracle.dot(xp, y)
+    assert abs(d - do) <= 1e-5 * abs(do)
+    ds = float(lift.dot(dev(x), dev(y)).item())  # signed: condition-scaled
+    dso = oracle.dot(x, y)
+    assert abs(ds - dso) <= 1e-5 * oracle.dot(np.abs(x), y)
+
+
+@pytest.mark.parametrize("n", [1, 9, 1000, RED_C + 1, 5 * RED_C + 3, 64 * RED_C + 1, 1 << 20])
+@pytest.mark.parametrize("off", [0, 1, 4])
+def test_integer_inputs_bit_exact(lift, n, off):
+    """Integer-valued inputs make every partial sum exact, so the result is unique:
+    this pins indexing, the tail, alignment handling and the cross-CTA fold."""
+    x = gen.host(n, 31, gen.TID_X, dist=gen.DIST_INT17)
+    y = gen.host(n, 31, gen.TID_Y, dist=gen.DIST_INT17)
+    xd, yd = at_offset(x, off), at_offset(y, (off * 3) % 8)
+    assert lift.asum(xd).item() == np.float32(oracle.asum(x))
+    assert lift.dot(xd, yd).item() == np.float32(oracle.dot(x, y))
+    assert lift.asum_partial(xd).item() == oracle.asum(x)
+    assert lift.dot_partial(xd, yd).item() == oracle.dot(x, y)
+
+
+def test_empty_reductions(lift):
+    e = torch.empty(0, dtype=torch.float32, device=DEV)
+    r = torch.full((1,), 7.0, device=DEV)
+    lift.asum(e, out=r)
+    assert bits(r)[0] == 0  # +0.0f
+    r.fill_(7.0)
+    lift.dot(e, e, out=r)
+    assert bits(r)[0] == 0
+    assert lift.asum_partial(e).item() == 0.0
+
+
+def test_determinism_runs_and_grids(lift):
+    n = 3 * 64 * RED_C + 12345
+    xd = dev(gen.host(n, 41, gen.TID_X))
+    yd = dev(gen.host(n, 41, gen.TID_Y))
+    base_a, base_d = bits(lift.asum(xd)), bits(lift.dot(xd, yd))
+    base_pa = lift.asum_partial(xd).item()
+    for _ in range(10):
+        assert np.array_equal(bits(lift.asum(xd)), base_a)
+        assert np.array_equal(bits(lift.dot(xd, yd)), base_d)
+    try:
+        for g in (1, 2, 3, 7, 148, 1000):
+            lift.set_grid_limit(g)
+            assert np.array_equal(bits(lift.asum(xd)), base_a), g
+            assert np.array_equal(bits(lift.dot(xd, yd)), base_d), g
+            assert lift.asum_partial(xd).item() == base_pa
+    finally:
+        lift.set_grid_limit(0)
+
+
+def test_alignment_does_not_change_bits(lift):
+    n = 2 * RED_C + 99
+    x = gen.host(n, 43, gen.TID_X)
+    y = gen.host(n, 43, gen.TID_Y)
+    ref_a = bits(lift.asum(at_offset(x, 0)))
+    ref_d = bits(lift.dot(at_offset(x, 0), at_offset(y, 0)))
+    for ox, oy in [(4, 4), (1, 1), (2, 5), (7, 0)]:
+        assert np.array_equal(bits(lift.asum(at_offset(x, ox))), ref_a)
+        assert np.array_equal(bits(lift.dot(at_offset(x, ox), at_offset(y, oy))), ref_d)
+
+
+def test_invariants(lift):
+    n = 200_001
+    x = gen.host(n, 51, gen.TID_X)
+    y = gen.host(n, 51, gen.TID_Y)
+    xd, yd = dev(x), dev(y)
+    assert np.array_equal(bits(lift.dot(xd, yd)), bits(lift.dot(yd, xd)))      # commutative
+    assert np.array_equal(bits(lift.asum(xd)), bits(lift.asum(-xd)))           # abs even
+    a = lift.asum(xd).item()
+    assert lift.asum(xd * 4.0).item() == 4.0 * a                                # 2^k scaling
+    xp = dev(np.abs(x))
+    assert np.array_equal(bits(lift.dot(xp, torch.ones_like(xp))), bits(lift.asum(xp)))
+
+
+@pytest.mark.parametrize("n,k", [(1 << 20, 3), (1 << 22, 10), (12345, 0)])
+def test_asum_plus_minus_c_closed_form_gpu(lift, n, k):
+    rng = np.random.default_rng(n + k)
+    c = 2.0 ** -k
+    x = np.where(rng.random(n) < 0.5, -c, c).astype(np.float32)
+    assert lift.asum(dev(x)).item() == np.float32(n * c)
+
+
+def test_workspace_ticket_reset(lift):
+    n = 64 * RED_C * 2 + 5
+    xd = dev(gen.host(n, 61, gen.TID_X))
+    ws = lift.Workspace(n, xd.device)
+    out = torch.empty(100, dtype=torch.float32, device=DEV)
+    for i in range(100):
+        lift.asum(xd, out=out[i:i + 1], ws=ws)
+    o = out.cpu().numpy()
+    assert np.all(o == o[0])
+    wf = ws.nbytes // 16 * 16
+    r = ((wf // 512 + 2) * 4 + 15) // 16 * 16  # tickets live in the last r bytes
+    assert torch.count_nonzero(ws.buf[wf - r:wf]).item() == 0
+
+
+def test_workspace_shared_across_sizes(lift):
+    """One workspace serves calls of different n in any order (tickets never clobbered)."""
+    ws = lift.Workspace(1 << 26, torch.device(DEV))
+    sizes = [1 << 26, 1 << 24, 3 * RED_C + 5, 1 << 22, 1 << 26, 100, 64 * RED_C * 5 + 1]
+    xs = {n: gen.host(n, 62, gen.TID_X, lo=0.0, hi=1.0) for n in set(sizes)}
+    for n in sizes:
+        g = lift.asum(dev(xs[n]), ws=ws).item()
+        o = oracle.asum(xs[n])
+        assert abs(g - o) <= 1e-5 * o, n
+
+
+def test_special_values_propagate(lift):
+    x = np.ones(70_000, np.float32)
+    x[12345] = np.nan
+    assert np.isnan(lift.asum(dev(x)).item())
+    x[12345] = -np.inf
+    assert lift.asum(dev(x)).item() == np.inf
+    big = np.full(1 << 20, 3e38, np.float32)  # fp64 partials: no overflow until the final RN
+    assert lift.asum(dev(big)).item() == np.inf
+    assert lift.asum_partial(dev(big)).item() == pytest.approx(3e38 * (1 << 20), rel=1e-6)
+
+
+def test_combine(lift):
+    p = torch.tensor([1.0, 2.0 ** -30, -1.0, 3.0, 0.5], dtype=torch.float64, device=DEV)
+    # pairwise over 8 leaves: ((1 + 2^-30) + (-1 + 3)) + (0.5 + 0) ...
+    assert lift.combine(p).item() == np.float32(3.5 + 2.0 ** -30)
+    one = torch.tensor([2.5], dtype=torch.float64, device=DEV)
+    assert lift.combine(one).item() == 2.5
+
+
+def test_sharded_partials_compose_bit_exactly(lift):
+    """Shards of a power-of-two number of groups combine to the unsharded bits."""
+    G = 64 * RED_C
+    n = 8 * G
+    x = gen.host(n, 71, gen.TID_X)
+    y = gen.host(n, 71, gen.TID_Y)
+    full_a = bits(lift.asum(dev(x)))
+    full_d = bits(lift.dot(dev(x), dev(y)))
+    for p in (2, 4, 8):
+        s = n // p
+        pa = torch.cat([lift.asum_partial(dev(x[r * s:(r + 1) * s])) for r in range(p)])
+        pd = torch.cat([lift.dot_partial(dev(x[r * s:(r + 1) * s]), dev(y[r * s:(r + 1) * s]))
+                        for r in range(p)])
+        assert np.array_equal(bits(lift.combine(pa)), full_a)
+        assert np.array_equal(bits(lift.combine(pd)), full_d)
+
+
+# ------------------------------------------------------------------------- gemv
+def gemv_inputs(m, n, seed, signed=False):
+    lo = -1.0 if signed else 0.0
+    A = gen.host(m * n, seed, gen.TID_A, lo=lo, hi=3.0 if not signed else 1.0).reshape(m, n)
+    x = gen.host(n, seed, gen.TID_X, lo=lo, hi=1.0)
+    y = gen.host(m, seed, gen.TID_Y, lo=lo, hi=2.0 if not signed else 1.0)
+    return A, x, y
+
+
+def check_gemv(got, A, x, y, alpha, beta):
+    ref = oracle.gemv(A, x, y, alpha, beta)
+    scale = abs(alpha) * (np.abs(A.astype(np.float64)) @ np.abs(x.astype(np.float64))) \
+        + abs(beta) * np.abs(y.astype(np.float64))
+    err = np.abs(got.astype(np.float64) - ref)
+    assert np.all(err <= 1e-6 * scale), float(np.max(err / np.maximum(scale, 1e-300)))
+    return ref
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 7), (8, 256), (17, 255), (301, 1027), (64, 4096),
+                                 (1000, 8192), (33, 16384), (20, 16385), (9, 40000), (3, 0)])
+def test_gemv_tolerance(lift, m, n):
+    A, x, y = gemv_inputs(m, n, m * 7 + n)
+    got = lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5).cpu().numpy()
+    ref = oracle.gemv(A, x, y, 1.5, 0.5)
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref))
+
+
+@pytest.mark.parametrize("m,n", [(37, 1029), (8, 20000)])
+def test_gemv_signed_condition_scaled(lift, m, n):
+    A, x, y = gemv_inputs(m, n, 5, signed=True)
+    got = lift.gemv(dev(A), dev(x), dev(y), -2.0, 0.75).cpu().numpy()
+    check_gemv(got, A, x, y, -2.0, 0.75)
+
+
+def test_gemv_identity_bit_exact(lift):
+    n = 4096 + 37
+    x = gen.host(n, 81, gen.TID_X)
+    y = gen.host(n, 81, gen.TID_Y)
+    eye = np.eye(n, dtype=np.float32)
+    got = lift.gemv(dev(eye), dev(x), dev(y), 1.5, 0.5).cpu().numpy()
+    exact = (1.5 * x.astype(np.float64) + 0.5 * y.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(got.view(np.uint32), exact.view(np.uint32))
+
+
+@pytest.mark.parametrize("pad", [0, 1, 3, 4, 8])
+def test_gemv_lda_and_alignment(lift, pad):
+    m, n = 70, 3000
+    A, x, y = gemv_inputs(m, n, 90 + pad)
+    buf = torch.zeros(m, n + pad, dtype=torch.float32, device=DEV)
+    buf[:, :n] = dev(A)
+    Av = buf[:, :n]
+    ref_bits = bits(lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5))
+    got = lift.gemv(Av, dev(x), dev(y), 1.5, 0.5)
+    assert np.array_equal(bits(got), ref_bits)  # load width never changes bits
+    off = torch.zeros(m * n + 3, dtype=torch.float32, device=DEV)[1:1 + m * n].view(m, n)
+    off.copy_(dev(A))
+    assert np.array_equal(bits(lift.gemv(off, dev(x), dev(y), 1.5, 0.5)), ref_bits)
+
+
+def test_gemv_in_place_and_zero_coeffs(lift):
+    m, n = 129, 513
+    A, x, y = gemv_inputs(m, n, 95)
+    yd = dev(y)
+    ref = oracle.gemv(A, x, y, 1.5, 0.5)
+    lift.gemv(dev(A), dev(x), yd, 1.5, 0.5, out=yd)
+    assert np.all(np.abs(yd.cpu().numpy() - ref) <= 1e-6 * np.abs(ref))
+    # beta = 0 still reads y (literal semantics, reading R11): NaN in y propagates
+    y2 = y.copy()
+    y2[3] = np.nan
+    got = lift.gemv(dev(A), dev(x), dev(y2), 1.0, 0.0).cpu().numpy()
+    assert np.isnan(got[3]) and not np.isnan(got[4])
+    got = lift.gemv(dev(A), dev(x), dev(y), 0.0, 1.0).cpu().numpy()
+    assert np.array_equal(got, y)
+
+
+def test_gemv_rows_independent_of_m(lift):
+    """A row's bits do not depend on m or on which rows share a launch (sharding)."""
+    m, n = 512, 2048 + 5
+    A, x, y = gemv_inputs(m, n, 97)
+    full = bits(lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5))
+    for a, b in [(0, 1), (100, 356), (511, 512), (256, 512)]:
+        part = bits(lift.gemv(dev(A[a:b]), dev(x), dev(y[a:b]), 1.5, 0.5))
+        assert np.array_equal(part, full[a:b])
+    try:
+        lift.set_grid_limit(3)
+        assert np.array_equal(bits(lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5)), full)
+    finally:
+        lift.set_grid_limit(0)
+
+
+# ------------------------------------------------- full BASELINE sizes (device inputs)
+def dev_gen(n, seed, tid, lo=-1.0, hi=1.0, dist=0):
+    t = torch.empty(n, dtype=torch.float32, device=DEV)
+    return gen.fill_device(t, seed, tid, 0, dist, lo, hi)
+
+
+def test_full_scal_2p28_sampled(lift):
+    n = 1 << 28
+    x = dev_gen(n, 0, gen.TID_X)
+    y = lift.scal(3.0, x)
+    idx = torch.tensor(np.r_[0:1000, n - 1000:n,
+                             np.random.default_rng(0).integers(0, n, 100_000)], device=DEV)
+    xs = x[idx].cpu().numpy()
+    assert np.array_equal(bits(y[idx]), oracle.scal(3.0, xs).astype(np.float32).view(np.uint32))
+    del x, y
+
+
+def test_full_asum_2p28(lift):
+    n = 1 << 28
+    x = dev_gen(n, 0, gen.TID_X)
+    g = lift.asum(x).item()
+    o = oracle.asum(gen.host(n, 0, gen.TID_X))
+    assert abs(g - o) <= 1e-5 * o
+
+
+@pytest.mark.parametrize("n", [1 << 24, 1 << 26])
+def test_full_dot(lift, n):
+    x = dev_gen(n, 0, gen.TID_X, 0.0, 1.0)
+    y = dev_gen(n, 0, gen.TID_Y, 0.0, 2.0)
+    g = lift.dot(x, y).item()
+    o = oracle.dot(gen.host(n, 0, gen.TID_X, lo=0.0, hi=1.0),
+                   gen.host(n, 0, gen.TID_Y, lo=0.0, hi=2.0))
+    assert abs(g - o) <= 1e-5 * o
+
+
+def test_full_gemv_8192(lift):
+    m = n = 8192
+    A = dev_gen(m * n, 0, gen.TID_A, 0.0, 3.0).view(m, n)
+    x = dev_gen(n, 0, gen.TID_X, 0.0, 1.0)
+    y = dev_gen(m, 0, gen.TID_Y, 0.0, 2.0)
+    got = lift.gemv(A, x, y, 1.5, 0.5).cpu().numpy()
+    ref = oracle.gemv(gen.host(m * n, 0, gen.TID_A, lo=0.0, hi=3.0).reshape(m, n),
+                      gen.host(n, 0, gen.TID_X, lo=0.0, hi=1.0),
+                      gen.host(m, 0, gen.TID_Y, lo=0.0, hi=2.0), 1.5, 0.5)
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref))
+
+
+def test_full_dot_2p31(lift):
+    """C5 at full size on one GPU (16 GiB of inputs); the oracle streams the same
+    seeded values from the host generator block by block."""
+    n = 1 << 31
+    x = dev_gen(n, 0, gen.TID_X, 0.0, 1.0)
+    y = dev_gen(n, 0, gen.TID_Y, 0.0, 2.0)
+    g = lift.dot(x, y).item()
+    del x, y
+    torch.cuda.empty_cache()
+    s = oracle.Stream()
+    blk = 1 << 25
+    xb = np.empty(blk, np.float32)
+    yb = np.empty(blk, np.float32)
+    for a in range(0, n, blk):
+        gen.fill_host(xb, 0, gen.TID_X, a, gen.DIST_UNIFORM, 0.0, 1.0)
+        gen.fill_host(yb, 0, gen.TID_Y, a, gen.DIST_UNIFORM, 0.0, 2.0)
+        s.dot(xb, yb)
+    o = s.value()
+    assert abs(g - o) <= 1e-5 * o
