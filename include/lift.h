@@ -65,6 +65,13 @@ typedef enum {
 #define LIFT_ABI_VERSION 1
 int lift_abi_version(void);
 
+/* The canonical decomposition that fixes the summation order of asum/dot (DESIGN.md
+ * reading R5): chunks of lift_reduce_chunk_elems() elements, folded in groups of
+ * lift_reduce_group_chunks() chunks.  Shards that are a power-of-two number of groups
+ * combine (lift_combine) to the same bits as the unsharded call. */
+int64_t lift_reduce_chunk_elems(void);
+int lift_reduce_group_chunks(void);
+
 /* Static, NUL-terminated description of a status code. */
 const char* lift_status_string(lift_status s);
 

@@ -52,6 +52,12 @@ def _out(out, n, dtype, device, name="out"):
     return out
 
 
+#: canonical reduction decomposition (lift_reduce_chunk_elems / _group_chunks)
+CHUNK_ELEMS = int(lib.lift_reduce_chunk_elems())
+GROUP_CHUNKS = int(lib.lift_reduce_group_chunks())
+GROUP_ELEMS = CHUNK_ELEMS * GROUP_CHUNKS
+
+
 def workspace_bytes(n: int) -> int:
     return int(lib.lift_workspace_bytes(int(n)))
 

@@ -15,7 +15,8 @@ LIB_PATH = os.environ.get("LIFT_LIB") or os.path.join(_HERE, "liblift.so")
 EXPORTS = (
     "lift_abi_version", "lift_status_string", "lift_workspace_bytes", "lift_scal",
     "lift_asum", "lift_dot", "lift_asum_partial", "lift_dot_partial", "lift_combine",
-    "lift_gemv", "lift_debug_set_grid_limit",
+    "lift_gemv", "lift_debug_set_grid_limit", "lift_reduce_chunk_elems",
+    "lift_reduce_group_chunks",
 )
 
 LIFT_OK = 0
@@ -43,6 +44,8 @@ def _load():
         "lift_combine": ([_int, _vp, _vp, _vp], _int),
         "lift_gemv": ([_i64, _i64, _f32, _vp, _i64, _vp, _f32, _vp, _vp, _vp], _int),
         "lift_debug_set_grid_limit": ([_int], _int),
+        "lift_reduce_chunk_elems": ([], _i64),
+        "lift_reduce_group_chunks": ([], _int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

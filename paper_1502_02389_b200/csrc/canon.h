@@ -10,9 +10,16 @@ namespace lift {
 // asum / dot (reduce.cuh)
 constexpr int RED_T = 256;                        // lanes per chunk (= threads per CTA)
 constexpr int RED_V = 8;                          // floats per vector slot (asVector^8)
-constexpr int RED_K = 16;                         // vectors per lane per chunk
-constexpr long long RED_C = (long long)RED_T * RED_V * RED_K;  // 32768 elements per chunk
-constexpr int RED_G = 64;                         // chunks per group (level-1 fold)
+#ifndef LIFT_RED_K
+#define LIFT_RED_K 4     // 8192-element chunks: short per-CTA work, fine-grained balance
+#endif
+#ifndef LIFT_RED_G
+#define LIFT_RED_G 256   // 2^21-element groups
+#endif
+constexpr int RED_K = LIFT_RED_K;                 // vectors per lane per chunk
+constexpr long long RED_C = (long long)RED_T * RED_V * RED_K;  // elements per chunk
+constexpr int RED_G = LIFT_RED_G;                 // chunks per group (level-1 fold)
+static_assert(RED_G <= RED_T, "group fold uses one leaf per thread");
 
 // gemv (gemv.cuh)
 constexpr int GEMV_T = 256;       // threads per CTA (8 warps)

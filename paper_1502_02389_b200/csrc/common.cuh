@@ -21,7 +21,7 @@ struct f8 {
 // 256-bit read-only streaming load (no L1 allocation): one asVector^8 element.
 __device__ __forceinline__ f8 ld_nc_v8(const float* p) {
     f8 r;
-    asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
           "=f"(r.v[6]), "=f"(r.v[7])
         : "l"(p));
@@ -118,6 +118,45 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
     }
+}
+
+// ---- Cluster Launch Control (sm_100): hardware work stealing -------------------------
+// A resident CTA cancels a not-yet-launched CTA of the same grid and takes over its
+// blockIdx (SASS UGETNEXTWORKID).  This gives persistent CTAs (per-CTA setup such as
+// gemv's x staging paid once) with the dynamic load balance of a one-CTA-per-unit grid.
+// Protocol: thread 0 issues clc_try_cancel early (before the current unit's work);
+// after the work, every thread calls clc_fetch; a __syncthreads must separate
+// clc_fetch from the next clc_try_cancel (the response buffer is reused).  After a
+// failed fetch the CTA must not issue another request.
+struct Clc {
+    uint4* resp;    // 16-byte response, shared memory
+    uint64_t* bar;  // mbarrier (count 1), shared memory
+    uint32_t phase;
+};
+
+__device__ __forceinline__ void clc_try_cancel(const Clc& c) {
+    mbar_arrive_expect_tx(c.bar, 16);
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 "
+        "[%0], [%1];" ::"r"(smem_u32(c.resp)),
+        "r"(smem_u32(c.bar))
+        : "memory");
+}
+
+// Returns true and the stolen CTA's blockIdx.x in `next`, or false (no work left).
+__device__ __forceinline__ bool clc_fetch(Clc& c, int64_t& next) {
+    mbar_wait(c.bar, c.phase);
+    c.phase ^= 1u;
+    uint32_t ok, cx;
+    asm volatile(
+        "{ .reg .b128 r; .reg .pred p; ld.shared.b128 r, [%2]; "
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r; selp.u32 %0, 1, 0, p; "
+        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r; }"
+        : "=r"(ok), "=r"(cx)
+        : "r"(smem_u32(c.resp))
+        : "memory");
+    next = cx;
+    return ok != 0;
 }
 
 }  // namespace lift

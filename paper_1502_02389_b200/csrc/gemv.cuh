@@ -44,7 +44,7 @@ struct GemvArgs {
 };
 
 __host__ __device__ constexpr size_t gemv_smem_bytes(int P) {
-    return 16 /*mbarrier*/ + (size_t)P * 4 /*fp32 stage*/ + (size_t)8 * (P / 8 + 1) * 8 /*fp64*/;
+    return 32 /*mbarrier*/ + (size_t)P * 4 /*fp32 stage*/ + (size_t)8 * (P / 8 + 1) * 8 /*fp64*/;
 }
 
 // Stage x[c0, c0+pc) into xs (fp64, slot-major).  Called by the whole CTA.
@@ -146,56 +146,57 @@ __device__ __forceinline__ void gemv_epilogue(const GemvArgs& a, const int64_t* 
     }
 }
 
-// MULTI = false: n <= P, x staged once, rows assigned per warp (no CTA syncs after
-// staging).  MULTI = true: n > P, rows assigned per CTA block, x re-staged per panel.
+// Row blocks: 8 warps x R rows.  Launch one CTA per row block; resident CTAs steal the
+// not-yet-launched ones with Cluster Launch Control, so x is staged once per resident
+// CTA while the hardware balances rows across SMs.
+// MULTI = false: n <= P, x staged once.  MULTI = true: n > P, x re-staged per panel.
 template <int R, int U, int LW, bool MULTI>
 __global__ void __launch_bounds__(GEMV_T) gemv_kernel(GemvArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    float* xstage = reinterpret_cast<float*>(smem + 16);
-    double* xs = reinterpret_cast<double*>(smem + 16 + (size_t)a.P * 4);
+    float* xstage = reinterpret_cast<float*>(smem + 32);
+    double* xs = reinterpret_cast<double*>(smem + 32 + (size_t)a.P * 4);
+    __shared__ __align__(16) uint4 clc_resp;
+    __shared__ __align__(8) uint64_t clc_bar;
     const int warp = threadIdx.x >> 5;
     uint32_t phase = 0;
-    if (threadIdx.x == 0) mbar_init(bar, 1);
+    Clc clc{&clc_resp, &clc_bar, 0};
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(&clc_bar, 1);
+    }
     __syncthreads();
+    if constexpr (!MULTI) gemv_stage_x(a, 0, (int)a.n, bar, xstage, xs, phase);
 
-    if constexpr (!MULTI) {
-        gemv_stage_x(a, 0, (int)a.n, bar, xstage, xs, phase);
-        const int64_t total_warps = (int64_t)gridDim.x * (GEMV_T / 32);
-        for (int64_t r0 = ((int64_t)blockIdx.x * (GEMV_T / 32) + warp) * R; r0 < a.m;
-             r0 += total_warps * R) {
-            int64_t rows[R];
+    constexpr int64_t rows_per_block = (int64_t)(GEMV_T / 32) * R;
+    int64_t blk = blockIdx.x;
+    while (true) {
+        if (threadIdx.x == 0) clc_try_cancel(clc);  // steal the next block while we work
+        const int64_t r0 = blk * rows_per_block + (int64_t)warp * R;
+        int64_t rows[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) rows[r] = min(r0 + r, a.m - 1);
-            double acc[R][8];
+        for (int r = 0; r < R; ++r) rows[r] = min(r0 + r, a.m - 1);
+        double acc[R][8];
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+        for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
-            gemv_panel<R, U, LW>(a, rows, 0, (int)a.n, xs, acc);
-            gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
-        }
-    } else {
-        const int64_t rows_per_block = (int64_t)(GEMV_T / 32) * R;
-        for (int64_t b0 = (int64_t)blockIdx.x * rows_per_block; b0 < a.m;
-             b0 += (int64_t)gridDim.x * rows_per_block) {
-            const int64_t r0 = b0 + (int64_t)warp * R;
-            int64_t rows[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) rows[r] = min(r0 + r, a.m - 1);
-            double acc[R][8];
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
+            for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
+        if constexpr (!MULTI) {
+            if (r0 < a.m) gemv_panel<R, U, LW>(a, rows, 0, (int)a.n, xs, acc);
+        } else {
             for (int64_t c0 = 0; c0 < a.n; c0 += a.P) {
                 const int pc = (int)min((int64_t)a.P, a.n - c0);
                 gemv_stage_x(a, c0, pc, bar, xstage, xs, phase);
-                gemv_panel<R, U, LW>(a, rows, c0, pc, xs, acc);
+                if (r0 < a.m) gemv_panel<R, U, LW>(a, rows, c0, pc, xs, acc);
                 __syncthreads();  // all warps done with xs before the next panel
             }
-            if (r0 < a.m) gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
         }
+        if (r0 < a.m) gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
+        int64_t next;
+        const bool more = clc_fetch(clc, next);
+        __syncthreads();  // everyone has read the response before it is reused
+        if (!more) break;
+        blk = next;
     }
 }
 

@@ -100,12 +100,20 @@ int occupancy(const void* fn, int threads, size_t smem) {
     return b;
 }
 
-int64_t grid_for(int64_t work_ctas, const void* fn, int threads, size_t smem) {
+#ifndef LIFT_PERSISTENT
+#define LIFT_PERSISTENT 0  // 1: grid capped at resident CTAs (grid-stride); 0: one CTA per unit
+#endif
+// `stealing`: the kernel takes further units by Cluster Launch Control instead of a
+// grid-stride loop, so its grid must cover all units (the test grid cap cannot apply).
+int64_t grid_for(int64_t work_ctas, const void* fn, int threads, size_t smem, bool persistent,
+                 bool stealing = false) {
     const int dev = current_device();
-    int64_t g = (int64_t)sm_count(dev) * occupancy(fn, threads, smem);
-    if (work_ctas < g) g = work_ctas;
+    int64_t g = work_ctas;
+    const int64_t resident = (int64_t)sm_count(dev) * occupancy(fn, threads, smem);  // also sets smem attr
+    if (persistent && resident < g) g = resident;
+    if (g > 0x7fffffffLL) g = 0x7fffffffLL;
     const int lim = g_grid_limit.load();
-    if (lim > 0 && g > lim) g = lim;
+    if (!stealing && lim > 0 && g > lim) g = lim;
     return g < 1 ? 1 : g;
 }
 
@@ -185,7 +193,7 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     const void* fn = lw == 8 ? (const void*)reduce_kernel<Op, 8, B>
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
                              : (const void*)reduce_kernel<Op, 1, B>;
-    const int64_t grid = grid_for(L.nc, fn, RED_T, 0);
+    const int64_t grid = grid_for(L.nc, fn, RED_T, 0, LIFT_PERSISTENT);
     if (lw == 8) reduce_kernel<Op, 8, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
     else if (lw == 4) reduce_kernel<Op, 4, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
     else reduce_kernel<Op, 1, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
@@ -210,7 +218,7 @@ lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
     const void* fn = (const void*)gemv_kernel<R, U, LW, MULTI>;
     const int64_t rows_per_cta = (int64_t)(GEMV_T / 32) * R;
     const int64_t work = (a.m + rows_per_cta - 1) / rows_per_cta;
-    const int64_t grid = grid_for(work, fn, GEMV_T, smem);
+    const int64_t grid = grid_for(work, fn, GEMV_T, smem, false, true);  // CLC steals
     gemv_kernel<R, U, LW, MULTI><<<(unsigned)grid, GEMV_T, smem, s>>>(a);
     return launched();
 }
@@ -223,6 +231,9 @@ using namespace lift;
 extern "C" {
 
 int lift_abi_version(void) { return LIFT_ABI_VERSION; }
+
+int64_t lift_reduce_chunk_elems(void) { return RED_C; }
+int lift_reduce_group_chunks(void) { return RED_G; }
 
 const char* lift_status_string(lift_status s) {
     switch (s) {
@@ -260,7 +271,7 @@ lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_str
     const bool alias = (x == y);
     const void* fn = lw == 8 ? scal_fn<8>(alias) : lw == 4 ? scal_fn<4>(alias) : scal_fn<1>(alias);
     const int64_t tile = (int64_t)SCAL_T * SCAL_U;
-    const int64_t grid = grid_for((nslots + tile - 1) / tile, fn, SCAL_T, 0);
+    const int64_t grid = grid_for((nslots + tile - 1) / tile, fn, SCAL_T, 0, LIFT_PERSISTENT);
     if (lw == 8) alias ? scal_go<8, true>(grid, nslots, (int)head, tail, alpha, x, y, s)
                        : scal_go<8, false>(grid, nslots, (int)head, tail, alpha, x, y, s);
     else if (lw == 4) alias ? scal_go<4, true>(grid, nslots, (int)head, tail, alpha, x, y, s)

@@ -86,9 +86,11 @@ __device__ __forceinline__ double cta_pairwise256(double v, double* wbuf) {
     return r;
 }
 
-template <class Op, int LW, int B>
+template <class Op, int LW, int B0>
 __device__ __forceinline__ void chunk_body_full(const float* xc, const float* yc,
                                                 typename Op::acc_t* acc) {
+    constexpr int B = B0 < RED_K ? B0 : RED_K;
+    static_assert(RED_K % B == 0, "load batch must divide RED_K");
     const int t = threadIdx.x;
 #pragma unroll
     for (int k0 = 0; k0 < RED_K; k0 += B) {

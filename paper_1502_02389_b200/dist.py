@@ -27,7 +27,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-GROUP_ELEMS = 64 * 32768  # RED_G * RED_C (csrc/canon.h)
+from . import GROUP_ELEMS  # noqa: E402  (RED_G * RED_C from liblift, csrc/canon.h)
 
 
 def shard_range(n: int, rank: int, world: int, align: int = GROUP_ELEMS) -> tuple[int, int]:

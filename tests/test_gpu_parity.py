@@ -18,7 +18,10 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 DEV = "cuda:0"
-RED_C = 32768  # canonical chunk (csrc/canon.h)
+from paper_1502_02389_b200._lib import lib as _abi  # noqa: E402
+
+RED_C = int(_abi.lift_reduce_chunk_elems())        # canonical chunk (csrc/canon.h)
+GROUP = RED_C * int(_abi.lift_reduce_group_chunks())  # canonical group
 
 
 @pytest.fixture(scope="module")
@@ -99,7 +102,7 @@ def test_scal_special_values(lift):
 
 # ------------------------------------------------------------------- asum / dot
 RED_SIZES = [1, 2, 7, 8, 9, 255, 256, 257, 4096, RED_C - 1, RED_C, RED_C + 1,
-             3 * RED_C + 17, 100_003, 64 * RED_C - 5, 64 * RED_C + 7, (1 << 22) + 3]
+             3 * RED_C + 17, 100_003, GROUP - 5, GROUP + 7, (1 << 22) + 3]
 
 
 @pytest.mark.parametrize("n", RED_SIZES)
@@ -118,7 +121,7 @@ def test_asum_dot_tolerance(lift, n):
     assert abs(ds - dso) <= 1e-5 * oracle.dot(np.abs(x), y)
 
 
-@pytest.mark.parametrize("n", [1, 9, 1000, RED_C + 1, 5 * RED_C + 3, 64 * RED_C + 1, 1 << 20])
+@pytest.mark.parametrize("n", [1, 9, 1000, RED_C + 1, 5 * RED_C + 3, GROUP + 1, 1 << 20])
 @pytest.mark.parametrize("off", [0, 1, 4])
 def test_integer_inputs_bit_exact(lift, n, off):
     """Integer-valued inputs make every partial sum exact, so the result is unique:
@@ -144,7 +147,7 @@ def test_empty_reductions(lift):
 
 
 def test_determinism_runs_and_grids(lift):
-    n = 3 * 64 * RED_C + 12345
+    n = 3 * GROUP + 12345
     xd = dev(gen.host(n, 41, gen.TID_X))
     yd = dev(gen.host(n, 41, gen.TID_Y))
     base_a, base_d = bits(lift.asum(xd)), bits(lift.dot(xd, yd))
@@ -195,7 +198,7 @@ def test_asum_plus_minus_c_closed_form_gpu(lift, n, k):
 
 
 def test_workspace_ticket_reset(lift):
-    n = 64 * RED_C * 2 + 5
+    n = GROUP * 2 + 5
     xd = dev(gen.host(n, 61, gen.TID_X))
     ws = lift.Workspace(n, xd.device)
     out = torch.empty(100, dtype=torch.float32, device=DEV)
@@ -211,7 +214,7 @@ def test_workspace_ticket_reset(lift):
 def test_workspace_shared_across_sizes(lift):
     """One workspace serves calls of different n in any order (tickets never clobbered)."""
     ws = lift.Workspace(1 << 26, torch.device(DEV))
-    sizes = [1 << 26, 1 << 24, 3 * RED_C + 5, 1 << 22, 1 << 26, 100, 64 * RED_C * 5 + 1]
+    sizes = [1 << 26, 1 << 24, 3 * RED_C + 5, 1 << 22, 1 << 26, 100, GROUP * 5 + 1]
     xs = {n: gen.host(n, 62, gen.TID_X, lo=0.0, hi=1.0) for n in set(sizes)}
     for n in sizes:
         g = lift.asum(dev(xs[n]), ws=ws).item()
@@ -240,7 +243,7 @@ def test_combine(lift):
 
 def test_sharded_partials_compose_bit_exactly(lift):
     """Shards of a power-of-two number of groups combine to the unsharded bits."""
-    G = 64 * RED_C
+    G = GROUP
     n = 8 * G
     x = gen.host(n, 71, gen.TID_X)
     y = gen.host(n, 71, gen.TID_Y)
