@@ -21,9 +21,7 @@ constexpr long long RED_C = (long long)RED_T * RED_V * RED_K;  // elements per c
 constexpr int RED_G = LIFT_RED_G;                 // chunks per group (level-1 fold)
 static_assert(RED_G <= RED_T, "group fold uses one leaf per thread");
 
-// gemv (gemv.cuh)
-constexpr int GEMV_T = 256;       // threads per CTA (8 warps)
-constexpr int GEMV_V = 8;         // floats per vector slot along a row
-constexpr int GEMV_PMAX = 16384;  // max x-panel columns staged in shared memory
+// gemv: the row order is defined in gemv.cuh (chunks of min(8192, round_up(n,1024))
+// columns, 8 warp segments, 4-float lane vectors, 4 fp64 lane accumulators).
 
 }  // namespace lift

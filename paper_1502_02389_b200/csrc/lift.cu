@@ -15,12 +15,6 @@
 #include "reduce.cuh"
 #include "scal.cuh"
 
-#ifndef LIFT_GEMV_R
-#define LIFT_GEMV_R 2  // rows per warp
-#endif
-#ifndef LIFT_GEMV_U
-#define LIFT_GEMV_U 4  // k-steps of loads in flight per row
-#endif
 #ifndef LIFT_ASUM_B
 #define LIFT_ASUM_B 8  // 256-bit loads in flight per lane (asum)
 #endif
@@ -211,15 +205,39 @@ const void* scal_fn(bool alias) {
     return alias ? (const void*)scal_kernel<LW, true> : (const void*)scal_kernel<LW, false>;
 }
 
-template <int LW, bool MULTI>
-lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
-    constexpr int R = LIFT_GEMV_R, U = LIFT_GEMV_U;
-    const size_t smem = gemv_smem_bytes(a.P);
-    const void* fn = (const void*)gemv_kernel<R, U, LW, MULTI>;
-    const int64_t rows_per_cta = (int64_t)(GEMV_T / 32) * R;
-    const int64_t work = (a.m + rows_per_cta - 1) / rows_per_cta;
-    const int64_t grid = grid_for(work, fn, GEMV_T, smem, false, true);  // CLC steals
-    gemv_kernel<R, U, LW, MULTI><<<(unsigned)grid, GEMV_T, smem, s>>>(a);
+lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
+    a.cw = gemv_chunk_width(a.n);
+    a.nchunks = (int)((a.n + a.cw - 1) / a.cw);
+    const uintptr_t aa = reinterpret_cast<uintptr_t>(a.A);
+    const bool vec4 = (aa & 15) == 0 && a.lda % 4 == 0;
+    const bool tma_ok = vec4 && a.n >= 4 && a.n % 4 == 0 && a.n <= GEMV_NMAX_TMA &&
+                        (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
+    if (tma_ok) {
+        a.xs_stride = (int)((a.n + 3) / 4) + 1;
+        const size_t fixed = GEMV_CTRL_BYTES + gemv_xs_bytes(a.xs_stride);
+        int stages = (int)((GEMV_SMEM_LIMIT - fixed) / gemv_stage_bytes(a.cw));
+        if (stages > GEMV_SMAX) stages = GEMV_SMAX;
+        // x is staged through the ring before streaming starts: it must fit there
+        if (stages >= 2 && (size_t)stages * gemv_stage_bytes(a.cw) >= (size_t)a.n * 4) {
+            a.stages = stages;
+            const size_t smem = fixed + (size_t)stages * gemv_stage_bytes(a.cw);
+            const void* fn = (const void*)gemv_tma_kernel;
+            const int64_t grid = grid_for(a.m, fn, (GEMV_WARPS + 1) * 32, smem, false, true);
+            gemv_tma_kernel<<<(unsigned)grid, (GEMV_WARPS + 1) * 32, smem, s>>>(a);
+            return launched();
+        }
+    }
+    a.xs_stride = 0;
+    a.stages = 0;
+    if (vec4) {
+        const int64_t grid = grid_for(a.m, (const void*)gemv_ldg_kernel<4>, GEMV_WARPS * 32, 0,
+                                      false, true);
+        gemv_ldg_kernel<4><<<(unsigned)grid, GEMV_WARPS * 32, 0, s>>>(a);
+    } else {
+        const int64_t grid = grid_for(a.m, (const void*)gemv_ldg_kernel<1>, GEMV_WARPS * 32, 0,
+                                      false, true);
+        gemv_ldg_kernel<1><<<(unsigned)grid, GEMV_WARPS * 32, 0, s>>>(a);
+    }
     return launched();
 }
 
@@ -337,18 +355,7 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
     a.x = x;
     a.y = y;
     a.y_out = y_out;
-    const bool multi = n > GEMV_PMAX;
-    a.P = multi ? GEMV_PMAX : (int)(((n > 0 ? n : 1) + 255) / 256 * 256);
-    a.xs_stride = a.P / 8 + 1;
-    const uintptr_t aa = reinterpret_cast<uintptr_t>(A);
-    const int lw = ((aa & 31) == 0 && lda % 8 == 0) ? 8 : ((aa & 15) == 0 && lda % 4 == 0) ? 4 : 1;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (multi) {
-        return lw == 8 ? gemv_go<8, true>(a, s) : lw == 4 ? gemv_go<4, true>(a, s)
-                                                          : gemv_go<1, true>(a, s);
-    }
-    return lw == 8 ? gemv_go<8, false>(a, s) : lw == 4 ? gemv_go<4, false>(a, s)
-                                                       : gemv_go<1, false>(a, s);
+    return gemv_launch(a, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
