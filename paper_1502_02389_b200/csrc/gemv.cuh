@@ -46,6 +46,14 @@ constexpr int GEMV_NMAX_TMA = 16384;          // x (fp64) must fit in shared mem
 constexpr int GEMV_SMAX = 6;                  // max ring stages
 constexpr int GEMV_SMEM_LIMIT = 227 * 1024;   // opt-in dynamic shared memory per CTA
 constexpr int GEMV_CTRL_BYTES = 1024;         // control block at the start of smem
+#ifndef LIFT_GEMV_RU
+#define LIFT_GEMV_RU 2   // rows per CLC work unit (gemv_tma)
+#endif
+#ifndef LIFT_GEMV_CLC_DEPTH
+#define LIFT_GEMV_CLC_DEPTH 3  // CLC steal requests kept in flight
+#endif
+constexpr int GEMV_RU = LIFT_GEMV_RU;
+constexpr int GEMV_CLC_DEPTH = LIFT_GEMV_CLC_DEPTH;
 
 struct GemvArgs {
     int64_t m, n, lda;
@@ -71,8 +79,8 @@ struct GemvCtrl {              // lives in the first GEMV_CTRL_BYTES of shared m
     uint64_t full[GEMV_SMAX];
     uint64_t empty[GEMV_SMAX];
     uint64_t xbar;
-    uint64_t clc_bar;
-    uint4 clc_resp;
+    uint64_t clc_bar[GEMV_CLC_DEPTH];
+    uint4 clc_resp[GEMV_CLC_DEPTH];
     int64_t meta_row[GEMV_SMAX];    // row of the chunk in a stage; -1 = no more work
     int meta_chunk[GEMV_SMAX];
     double rowpart[8][GEMV_WARPS];  // warp values of up to 8 rows in flight
@@ -84,10 +92,12 @@ __device__ __forceinline__ double pairwise4(const double* v) {
     return __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]));
 }
 
-// Row value and epilogue from the 8 warp values (fixed pairwise order).
-__device__ __forceinline__ void gemv_finish_row(const GemvArgs& a, int64_t row, const double* wv) {
+// Row value and epilogue from the 8 warp values (fixed pairwise order); yrow = y[row]
+// (loaded early by the caller so the epilogue never waits on global memory).
+__device__ __forceinline__ void gemv_finish_row(const GemvArgs& a, int64_t row, const double* wv,
+                                                float yrow) {
     const double d = pairwise8(wv);
-    const double w = __dmul_rn((double)a.beta, (double)a.y[row]);  // scal(b, y): exact
+    const double w = __dmul_rn((double)a.beta, (double)yrow);  // scal(b, y): exact
     a.y_out[row] = __double2float_rn(__fma_rn((double)a.alpha, d, w));
 }
 
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__((GEMV_WARPS + 1) * 32, 1) gemv_tma_kernel(Gemv
             mbar_init(&C.empty[s], GEMV_WARPS);
         }
         mbar_init(&C.xbar, 1);
-        mbar_init(&C.clc_bar, 1);
+        for (int q = 0; q < GEMV_CLC_DEPTH; ++q) mbar_init(&C.clc_bar[q], 1);
         for (int r = 0; r < 8; ++r) C.rowcnt[r] = 0;
     }
     __syncthreads();
@@ -165,29 +175,48 @@ __global__ void __launch_bounds__((GEMV_WARPS + 1) * 32, 1) gemv_tma_kernel(Gemv
     }
 
     if (warp == GEMV_WARPS) {
-        // ============ producer: one lane streams row chunks, steals rows by CLC =======
+        // ============ producer: one lane streams row chunks, steals units by CLC ======
+        // A unit is GEMV_RU consecutive rows.  GEMV_CLC_DEPTH steal requests stay in
+        // flight (one response buffer + mbarrier each) so the CLC round trip hides
+        // behind several units of streaming.  Requests are only issued before a failure
+        // has been observed; after one, the outstanding ones are drained and we stop.
         if (lane == 0) {
-            Clc clc{&C.clc_resp, &C.clc_bar, 0};
-            int64_t row = blockIdx.x;
+            Clc clc[GEMV_CLC_DEPTH];
+            for (int q = 0; q < GEMV_CLC_DEPTH; ++q) {
+                clc[q] = Clc{&C.clc_resp[q], &C.clc_bar[q], 0};
+                clc_try_cancel(clc[q]);
+            }
+            int64_t unit = blockIdx.x;
             uint32_t it = 0;
+            int q = 0;
             while (true) {
-                clc_try_cancel(clc);  // ask for the next row while this one streams
-                for (int c = 0; c < a.nchunks; ++c) {
-                    const int s = (int)(it % S);
-                    const uint32_t k = it / S;
-                    if (k > 0) mbar_wait(&C.empty[s], (k - 1) & 1);
-                    const int64_t c0 = (int64_t)c * a.cw;
-                    const uint32_t bytes = (uint32_t)min((int64_t)a.cw, a.n - c0) * 4u;
-                    C.meta_row[s] = row;
-                    C.meta_chunk[s] = c;
-                    mbar_arrive_expect_tx(&C.full[s], bytes);
-                    bulk_g2s(ring + (size_t)s * stage_floats, a.A + row * a.lda + c0, bytes,
-                             &C.full[s]);
-                    ++it;
+                const int64_t r_end = min((unit + 1) * GEMV_RU, a.m);
+                for (int64_t row = unit * GEMV_RU; row < r_end; ++row) {
+                    for (int c = 0; c < a.nchunks; ++c) {
+                        const int s = (int)(it % S);
+                        const uint32_t k = it / S;
+                        if (k > 0) mbar_wait(&C.empty[s], (k - 1) & 1);
+                        const int64_t c0 = (int64_t)c * a.cw;
+                        const uint32_t bytes = (uint32_t)min((int64_t)a.cw, a.n - c0) * 4u;
+                        C.meta_row[s] = row;
+                        C.meta_chunk[s] = c;
+                        mbar_arrive_expect_tx(&C.full[s], bytes);
+                        bulk_g2s(ring + (size_t)s * stage_floats, a.A + row * a.lda + c0, bytes,
+                                 &C.full[s]);
+                        ++it;
+                    }
                 }
                 int64_t next;
-                if (!clc_fetch(clc, next)) break;
-                row = next;
+                if (!clc_fetch(clc[q], next)) {
+                    for (int d = 1; d < GEMV_CLC_DEPTH; ++d) {  // drain the others
+                        int64_t ignored;
+                        clc_fetch(clc[(q + d) % GEMV_CLC_DEPTH], ignored);
+                    }
+                    break;
+                }
+                clc_try_cancel(clc[q]);  // re-arm this slot
+                q = (q + 1) % GEMV_CLC_DEPTH;
+                unit = next;
             }
             const int s = (int)(it % S);  // termination token
             const uint32_t k = it / S;
@@ -199,16 +228,46 @@ __global__ void __launch_bounds__((GEMV_WARPS + 1) * 32, 1) gemv_tma_kernel(Gemv
     }
 
     // ==================== consumers: 8 warps, one column segment each ================
+    // Single-chunk rows (n <= 8192) with a full segment: this warp's x values never
+    // change, so they live in registers (nv <= 8 vectors x 4 fp64) and the per-row
+    // shared-memory traffic is A only.
+    const int sw = a.cw / GEMV_WARPS, nv = sw / 128;
+    const bool xreg = a.nchunks == 1 && (int64_t)(warp + 1) * sw <= a.n;
+    double xr[8][4];
+    if (xreg) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k < nv) {
+                const int q = (warp * sw) / 4 + lane + 32 * k;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) xr[k][e] = xs[e * a.xs_stride + q];
+            }
+    }
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     uint32_t it = 0;
     int rowslot = 0;
+    float yrow = 0.f;
     while (true) {
         const int s = (int)(it % S);
         mbar_wait(&C.full[s], (it / S) & 1);
         const int64_t row = C.meta_row[s];
         if (row < 0) break;
         const int c = C.meta_chunk[s];
-        gemv_fold_stage(a, ring + (size_t)s * stage_floats, (int64_t)c * a.cw, xs, acc);
+        if (c == 0 && lane == 0) yrow = __ldg(a.y + row);  // prefetch for the epilogue
+        if (xreg) {  // same order as gemv_fold_stage, x from registers
+            const float* sa = ring + (size_t)s * stage_floats + warp * sw;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k < nv) {
+                    const float4 v = *reinterpret_cast<const float4*>(sa + 4 * (lane + 32 * k));
+                    acc[0] = __fma_rn((double)v.x, xr[k][0], acc[0]);
+                    acc[1] = __fma_rn((double)v.y, xr[k][1], acc[1]);
+                    acc[2] = __fma_rn((double)v.z, xr[k][2], acc[2]);
+                    acc[3] = __fma_rn((double)v.w, xr[k][3], acc[3]);
+                }
+        } else {
+            gemv_fold_stage(a, ring + (size_t)s * stage_floats, (int64_t)c * a.cw, xs, acc);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&C.empty[s]);
         ++it;
@@ -225,7 +284,7 @@ __global__ void __launch_bounds__((GEMV_WARPS + 1) * 32, 1) gemv_tma_kernel(Gemv
                     for (int w = 0; w < GEMV_WARPS; ++w)
                         v8[w] = *((volatile double*)&C.rowpart[rowslot][w]);
                     C.rowcnt[rowslot] = 0;
-                    gemv_finish_row(a, row, v8);
+                    gemv_finish_row(a, row, v8, yrow);
                 }
             }
             rowslot = (rowslot + 1) & 7;
@@ -247,7 +306,11 @@ __global__ void __launch_bounds__(GEMV_WARPS * 32) gemv_ldg_kernel(GemvArgs a) {
     const int sw = a.cw / GEMV_WARPS, nv = sw / 128;
     int64_t row = blockIdx.x;
     while (true) {
-        if (threadIdx.x == 0) clc_try_cancel(clc);
+        float yrow = 0.f;
+        if (threadIdx.x == 0) {
+            clc_try_cancel(clc);
+            yrow = __ldg(a.y + row);
+        }
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         const float* ar = a.A + row * a.lda;
         for (int c = 0; c < a.nchunks; ++c) {
@@ -274,7 +337,7 @@ __global__ void __launch_bounds__(GEMV_WARPS * 32) gemv_ldg_kernel(GemvArgs a) {
         const double v = warp_pairwise(pairwise4(acc));
         if (lane == 0) wv[w] = v;
         __syncthreads();
-        if (threadIdx.x == 0) gemv_finish_row(a, row, wv);
+        if (threadIdx.x == 0) gemv_finish_row(a, row, wv, yrow);
         int64_t next;
         const bool more = clc_fetch(clc, next);
         __syncthreads();  // wv and the CLC response are reused next step

@@ -21,8 +21,11 @@
 #ifndef LIFT_DOT_B
 #define LIFT_DOT_B 4   // vector pairs in flight per lane (dot)
 #endif
-#ifndef LIFT_RED_ACC
-#define LIFT_RED_ACC double  // per-lane accumulator of asum/dot (canonical order, R13)
+#ifndef LIFT_ASUM_ACC
+#define LIFT_ASUM_ACC float   // per-lane accumulators (canonical order, reading R13)
+#endif
+#ifndef LIFT_DOT_ACC
+#define LIFT_DOT_ACC double
 #endif
 
 namespace lift {
@@ -84,8 +87,10 @@ int occupancy(const void* fn, int threads, size_t smem) {
     for (int i = 0; i < g_nocc; ++i)
         if (g_occ[i].fn == fn && g_occ[i].dev == dev && g_occ[i].smem == smem)
             return g_occ[i].blocks;
+    // The attribute is a per-function maximum: set it to the largest opt-in size once,
+    // so launches with any smaller dynamic smem (other n) stay valid.
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMV_SMEM_LIMIT);
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess ||
         b < 1)
@@ -222,7 +227,8 @@ lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
             a.stages = stages;
             const size_t smem = fixed + (size_t)stages * gemv_stage_bytes(a.cw);
             const void* fn = (const void*)gemv_tma_kernel;
-            const int64_t grid = grid_for(a.m, fn, (GEMV_WARPS + 1) * 32, smem, false, true);
+            const int64_t units = (a.m + GEMV_RU - 1) / GEMV_RU;
+            const int64_t grid = grid_for(units, fn, (GEMV_WARPS + 1) * 32, smem, false, true);
             gemv_tma_kernel<<<(unsigned)grid, (GEMV_WARPS + 1) * 32, smem, s>>>(a);
             return launched();
         }
@@ -302,28 +308,28 @@ lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_str
 lift_status lift_asum(int64_t n, const float* x, float* result, void* ws, size_t ws_bytes,
                       lift_stream_t stream) {
     if (!result) return LIFT_ERR_NULL_POINTER;
-    return reduce_launch<AsumOp<LIFT_RED_ACC>, LIFT_ASUM_B>(n, x, nullptr, result, nullptr, ws, ws_bytes,
+    return reduce_launch<AsumOp<LIFT_ASUM_ACC>, LIFT_ASUM_B>(n, x, nullptr, result, nullptr, ws, ws_bytes,
                                               reinterpret_cast<cudaStream_t>(stream));
 }
 
 lift_status lift_dot(int64_t n, const float* x, const float* y, float* result, void* ws,
                      size_t ws_bytes, lift_stream_t stream) {
     if (!result) return LIFT_ERR_NULL_POINTER;
-    return reduce_launch<DotOp<LIFT_RED_ACC>, LIFT_DOT_B>(n, x, y, result, nullptr, ws, ws_bytes,
+    return reduce_launch<DotOp<LIFT_DOT_ACC>, LIFT_DOT_B>(n, x, y, result, nullptr, ws, ws_bytes,
                                             reinterpret_cast<cudaStream_t>(stream));
 }
 
 lift_status lift_asum_partial(int64_t n, const float* x, double* partial, void* ws,
                               size_t ws_bytes, lift_stream_t stream) {
     if (!partial) return LIFT_ERR_NULL_POINTER;
-    return reduce_launch<AsumOp<LIFT_RED_ACC>, LIFT_ASUM_B>(n, x, nullptr, nullptr, partial, ws, ws_bytes,
+    return reduce_launch<AsumOp<LIFT_ASUM_ACC>, LIFT_ASUM_B>(n, x, nullptr, nullptr, partial, ws, ws_bytes,
                                               reinterpret_cast<cudaStream_t>(stream));
 }
 
 lift_status lift_dot_partial(int64_t n, const float* x, const float* y, double* partial,
                              void* ws, size_t ws_bytes, lift_stream_t stream) {
     if (!partial) return LIFT_ERR_NULL_POINTER;
-    return reduce_launch<DotOp<LIFT_RED_ACC>, LIFT_DOT_B>(n, x, y, nullptr, partial, ws, ws_bytes,
+    return reduce_launch<DotOp<LIFT_DOT_ACC>, LIFT_DOT_B>(n, x, y, nullptr, partial, ws, ws_bytes,
                                             reinterpret_cast<cudaStream_t>(stream));
 }
 

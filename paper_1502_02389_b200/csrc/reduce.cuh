@@ -8,23 +8,24 @@
 // with the device-specific structure of Fig. 7a/7b re-designed for B200:
 //
 //  R2 split^C + reorder-stride: the input is cut into canonical chunks
-//     of RED_C = 2^15 elements.  Inside a chunk, lane t of RED_T = 256 owns the
+//     of RED_C = RED_T * 8 * RED_K elements (8192).  Inside a chunk, lane t of RED_T = 256 owns the
 //     8-float vectors t, t+256, t+512, ... (reorder-stride with s = 256), so a warp
 //     reads 32 consecutive 32-byte vectors per instruction (LDG.256, coalesced).
 //     Chunks go to CTAs grid-stride (map-workgroup).
 //  R1 fused reduce-seq o map-seq (rule 5f): each lane keeps 8
 //     accumulators (one per vector slot e) and folds acc_e = acc_e + |x| (asum) or
-//     acc_e = fma(x, y, acc_e) (dot) over its 16 vectors in ascending order — no
+//     acc_e = fma(x, y, acc_e) (dot) over its RED_K vectors in ascending order — no
 //     intermediate array.
 //  R3 toLocal + iterate(split-2 reduce): lane value = fixed pairwise
 //     fold of its 8 accumulators in fp64; warp butterfly (xor 1,2,4,8,16); then the
-//     8 warp values pairwise through shared memory -> one fp64 CHUNK PARTIAL.
+//     8 warp values pairwise through shared memory -> one fp64 CHUNK PARTIAL.  One
+//     CTA barrier per chunk; everything after it runs in warp 0 only.
 //  R4 the outermost reduce-seq o join, single pass, no second launch: a
 //     two-level last-block-done.  The CTA that finishes the last chunk of a group of
-//     RED_G = 64 chunks folds that group's partials (pairwise); the CTA that
-//     finishes the last group folds the group partials (pairwise, zero-padded to a
-//     power of two) and writes the fp32 result (rounded once) and/or the fp64
-//     partial.  Tickets are reset to 0 by the CTAs that consume them.
+//     RED_G chunks folds that group's partials (pairwise); the CTA that finishes the
+//     last group folds the group partials (pairwise, zero-padded to a power of two)
+//     and writes the fp32 result (rounded once) and/or the fp64 partial.  Tickets
+//     are reset to 0 by the CTAs that consume them.
 //
 // Determinism: every addition above happens in an order that is a pure function of
 // n (chunk, lane, slot, group indices) — never of the grid size, the SM count,
@@ -38,13 +39,19 @@
 
 namespace lift {
 
-// The fused per-element step (rule 5f).  Acc is the per-lane accumulator type: fp32
-// (the paper-era choice; overflows to Inf if a 16-term lane run exceeds FLT_MAX) or
-// fp64 (exact products, no overflow for any finite fp32 input; the default — see
-// DESIGN.md reading R13 and the measured cost in profiles/).
+// The fused per-element step (rule 5f).  Acc is the per-lane accumulator type.
+//  * asum uses fp32 accumulators over its RED_K = 4-term runs (|x| is exact, so only
+//    4-term rounding) — no fp32->fp64 conversion per element.  A run can only
+//    overflow if terms approach FLT_MAX/4; then the chunk is recomputed with fp64
+//    accumulators (see reduce_kernel), so results never differ from the fp64 fold by
+//    more than rounding and Inf/NaN inputs still propagate.
+//  * dot uses fp64 accumulators with exact products (an fp32 product could overflow
+//    or lose bits to underflow); reading R13.
 template <class Acc>
 struct AsumOp {
     using acc_t = Acc;
+    template <class A2>
+    using rebind = AsumOp<A2>;
     static constexpr bool kTwoInputs = false;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float) {
         if constexpr (sizeof(Acc) == 8) return __dadd_rn(acc, fabs((double)a));
@@ -54,6 +61,8 @@ struct AsumOp {
 template <class Acc>
 struct DotOp {
     using acc_t = Acc;
+    template <class A2>
+    using rebind = DotOp<A2>;
     static constexpr bool kTwoInputs = true;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float b) {
         if constexpr (sizeof(Acc) == 8) return __fma_rn((double)a, (double)b, acc);  // exact product
@@ -74,16 +83,31 @@ struct ReduceArgs {
     double* out_f64;     // may be null
 };
 
-// Pairwise fold of 256 per-thread values (warp butterfly, then 8 warps pairwise).
-// Result valid in thread 0.  `wbuf` holds 8 doubles in shared memory.
-__device__ __forceinline__ double cta_pairwise256(double v, double* wbuf) {
-    v = warp_pairwise(v);
-    if ((threadIdx.x & 31) == 0) wbuf[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double r = 0.0;
-    if (threadIdx.x == 0) r = pairwise8(wbuf);
-    __syncthreads();  // wbuf may be reused after this
-    return r;
+// Warp-level pairwise fold of `nleaf` fp64 leaves read from global memory (L2),
+// zero-padded to a power of two p2: lane l folds the aligned block [l*blk, (l+1)*blk)
+// (blk = max(1, p2/32)) with a binary-counter stack — the pairwise tree restricted to
+// that block — and the butterfly joins the 32 blocks.  Any such decomposition into
+// aligned power-of-two blocks yields exactly THE pairwise tree over the leaves.
+__device__ __forceinline__ double warp_fold_leaves(const double* leaves, int64_t nleaf) {
+    const int lane = threadIdx.x & 31;
+    int64_t p2 = 1;
+    while (p2 < nleaf) p2 <<= 1;
+    const int64_t blk = p2 > 32 ? p2 / 32 : 1;
+    double v;
+    if (blk == 1) {
+        v = (lane < nleaf) ? __ldcg(leaves + lane) : 0.0;
+    } else {
+        double stk[40];
+        int top = 0;
+        for (int64_t i = 0; i < blk; ++i) {
+            const int64_t li = (int64_t)lane * blk + i;
+            double w = (li < nleaf) ? __ldcg(leaves + li) : 0.0;
+            for (int64_t cnt = i; cnt & 1; cnt >>= 1) w = __dadd_rn(stk[--top], w);
+            stk[top++] = w;
+        }
+        v = stk[0];
+    }
+    return warp_pairwise(v);
 }
 
 template <class Op, int LW, int B0>
@@ -127,11 +151,11 @@ __device__ __forceinline__ void chunk_body_tail(const float* xc, const float* yc
 
 template <class Op, int LW, int B>
 __global__ void __launch_bounds__(RED_T) reduce_kernel(ReduceArgs a) {
-    __shared__ double wbuf[RED_T / 32];
-    __shared__ int s_last_chunk, s_last_group;
-    const int t = threadIdx.x;
+    __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int parity = 0;
 
-    for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x) {
+    for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x, parity ^= 1) {
         // ---- R1/R2: fused per-lane fold over the chunk ---------------------------
         const int64_t base = c * RED_C;
         const float* xc = a.x + base;
@@ -139,66 +163,66 @@ __global__ void __launch_bounds__(RED_T) reduce_kernel(ReduceArgs a) {
         typename Op::acc_t acc[RED_V];
 #pragma unroll
         for (int e = 0; e < RED_V; ++e) acc[e] = 0;
-        if (base + RED_C <= a.n) chunk_body_full<Op, LW, B>(xc, yc, acc);
+        const bool full = base + RED_C <= a.n;
+        if (full) chunk_body_full<Op, LW, B>(xc, yc, acc);
         else chunk_body_tail<Op>(xc, yc, a.n - base, acc);
 
-        // ---- R3: lane -> warp -> CTA, fixed pairwise, fp64 -----------------------
+        // ---- R3: lane -> warp (butterfly) -> CTA (8 warps pairwise), fp64 --------
         double lane8[RED_V];
+        bool bad = false;
 #pragma unroll
-        for (int e = 0; e < RED_V; ++e) lane8[e] = (double)acc[e];
-        const double part = cta_pairwise256(pairwise8(lane8), wbuf);
+        for (int e = 0; e < RED_V; ++e) {
+            lane8[e] = (double)acc[e];
+            if constexpr (sizeof(acc[0]) == 4) bad |= !isfinite(acc[e]);
+        }
+        double wv = warp_pairwise(pairwise8(lane8));
+        if (lane == 0) wbuf[parity][warp] = wv;
+        bool redo = false;
+        if constexpr (sizeof(acc[0]) == 4) redo = __syncthreads_or(bad);  // the one barrier
+        else __syncthreads();
+        if constexpr (sizeof(acc[0]) == 4) {
+            if (redo) {  // rare: an fp32 run overflowed (or the chunk holds Inf/NaN)
+                using Op64 = typename Op::template rebind<double>;
+                double acc64[RED_V];
+#pragma unroll
+                for (int e = 0; e < RED_V; ++e) acc64[e] = 0.0;
+                if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64);
+                else chunk_body_tail<Op64>(xc, yc, a.n - base, acc64);
+                wv = warp_pairwise(pairwise8(acc64));
+                if (lane == 0) wbuf[parity][warp] = wv;  // nobody reads wbuf before the barrier
+                __syncthreads();
+            }
+        }
+        if (warp != 0) continue;
 
-        // ---- R4 level 1: publish the chunk partial, group ticket -----------------
+        // ---- R4, warp 0 only: publish the chunk partial, group ticket ------------
         const int64_t g = c / RED_G;
-        if (t == 0) {
-            a.chunk_part[c] = part;
+        unsigned last = 0;
+        if (lane == 0) {
+            a.chunk_part[c] = pairwise8(wbuf[parity]);
             __threadfence();
             const int64_t gcount = min((int64_t)RED_G, a.nc - g * RED_G);
-            const unsigned old = atomicAdd(&a.tick[g], 1u);
-            s_last_chunk = (old == (unsigned)(gcount - 1));
+            last = (atomicAdd(&a.tick[g], 1u) == (unsigned)(gcount - 1));
         }
-        __syncthreads();
-        if (!s_last_chunk) continue;  // uniform across the CTA
+        if (!__shfl_sync(0xffffffffu, last, 0)) continue;
 
-        // This CTA finished the group's last chunk: fold the group (pairwise over
-        // RED_G leaves; RED_G <= RED_T so one leaf per thread, missing ones = 0).
+        // Last chunk of group g: fold the group's RED_G chunk partials (pairwise).
         __threadfence();
-        const int64_t leaf = g * RED_G + t;
-        double v = (t < RED_G && leaf < a.nc) ? __ldcg(&a.chunk_part[leaf]) : 0.0;
-        const double gpart = cta_pairwise256(v, wbuf);
-        if (t == 0) {
+        const int64_t g0 = g * RED_G;
+        const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
+        last = 0;
+        if (lane == 0) {
             a.group_part[g] = gpart;
             a.tick[g] = 0u;  // reset for the next call (workspace contract)
             __threadfence();
-            const unsigned old = atomicAdd(&a.tick[a.ng], 1u);
-            s_last_group = (old == (unsigned)(a.ng - 1));
+            last = (atomicAdd(&a.tick[a.ng], 1u) == (unsigned)(a.ng - 1));
         }
-        __syncthreads();
-        if (!s_last_group) continue;
+        if (!__shfl_sync(0xffffffffu, last, 0)) continue;
 
-        // ---- R4 level 2: final fold over all group partials ----------------------
+        // Last group: final pairwise fold over the group partials, round once.
         __threadfence();
-        int64_t p2 = 1;
-        while (p2 < a.ng) p2 <<= 1;
-        double tv;
-        if (p2 <= RED_T) {
-            tv = (t < a.ng) ? __ldcg(&a.group_part[t]) : 0.0;
-        } else {
-            // Thread t folds the aligned block [t*blk, (t+1)*blk) pairwise with a
-            // binary-counter stack, so the overall fold is the pairwise tree.
-            const int64_t blk = p2 / RED_T;
-            double stk[40];
-            int top = 0;
-            for (int64_t i = 0; i < blk; ++i) {
-                const int64_t li = (int64_t)t * blk + i;
-                double w = (li < a.ng) ? __ldcg(&a.group_part[li]) : 0.0;
-                for (int64_t cnt = i; cnt & 1; cnt >>= 1) w = __dadd_rn(stk[--top], w);
-                stk[top++] = w;
-            }
-            tv = stk[0];
-        }
-        const double total = cta_pairwise256(tv, wbuf);
-        if (t == 0) {
+        const double total = warp_fold_leaves(a.group_part, a.ng);
+        if (lane == 0) {
             if (a.out_f64) *a.out_f64 = total;
             if (a.out_f32) *a.out_f32 = __double2float_rn(total);
             a.tick[a.ng] = 0u;

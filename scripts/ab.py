@@ -43,21 +43,25 @@ def child(reps=30):
         "asum_2p20": (lambda: lift.asum(x[:1 << 20], out=r, ws=ws), 4 << 20),
     }
     out = {}
-    for name, (fn, nbytes) in ops.items():
+    samples = {name: [] for name in ops}
+    for name, (fn, _) in ops.items():
         for _ in range(5):
             fn()
-        ts = []
-        for _ in range(3):  # 3 trials of `reps` back-to-back launches; keep the median
+    torch.cuda.synchronize()
+    for _ in range(5):  # rounds interleaved across ops; each = `reps` back-to-back launches
+        for name, (fn, nbytes) in ops.items():
             s, e = torch.cuda.Event(True), torch.cuda.Event(True)
             s.record()
             for _ in range(reps):
                 fn()
             e.record()
             e.synchronize()
-            ts.append(s.elapsed_time(e) / reps)
-        ts.sort()
-        med = ts[1]
-        out[name] = {"us": round(med * 1e3, 2), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1)}
+            samples[name].append(s.elapsed_time(e) / reps)
+    for name, (fn, nbytes) in ops.items():
+        ts = sorted(samples[name])
+        med = ts[len(ts) // 2]
+        out[name] = {"us": round(med * 1e3, 2), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1),
+                     "spread%": round(100 * (ts[-1] - ts[0]) / med, 1)}
     print(json.dumps(out))
 
 

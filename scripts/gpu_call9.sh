@@ -1,0 +1,9 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
+timeout 600 python scripts/ab.py build/liblift_cur.so > gpurun_out/ab9.log 2>&1
+cat gpurun_out/ab9.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"gemv_tma|reduce_kernel" -s 3 -c 3 -o gpurun_out/r1b_full python scripts/ncu_probe.py 2 > gpurun_out/r1b_ncu.log 2>&1
+echo "ncu rc=$?"
