@@ -45,6 +45,10 @@ def lib():
                                   ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                   ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_gemv.restype = None
+        L.oracle_blackscholes.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_blackscholes.restype = None
         L.oracle_finish.argtypes = [ctypes.c_void_p]
         L.oracle_finish.restype = ctypes.c_double
         _lib = L
@@ -117,3 +121,13 @@ def gemv(A, x, y, alpha: float, beta: float) -> np.ndarray:
     lib().oracle_gemv(m, n, np.float32(alpha), A.ctypes.data, lda, x.ctypes.data,
                       np.float32(beta), y.ctypes.data, out.ctypes.data)
     return out
+
+
+def blackscholes(s, K: float, r: float, v: float, T: float):
+    """Fig. 9 map(BSComputation, s): fp64 (call, put) per stock price."""
+    s = _f32(s)
+    call = np.empty(s.size, np.float64)
+    put = np.empty(s.size, np.float64)
+    lib().oracle_blackscholes(s.size, s.ctypes.data, float(K), float(r), float(v), float(T),
+                              call.ctypes.data, put.ctypes.data)
+    return call, put

@@ -110,3 +110,31 @@ void oracle_gemv(int64_t m, int64_t n, float a, const float *A, int64_t lda,
         out[i] = z + w;
     }
 }
+
+/* ---------------------------------------------------------------- BlackScholes
+ * NEXT-3 row.  Fig. 9:
+ *     BSComputation(s) = d1 = compD1(s); d2 = compD2(d1, s)
+ *                        return { compCall(d1, d2, s), compPut(d1, d2, s) }
+ *     blackScholes(s)  = map(BSComputation, s)
+ * The helper bodies are "not shown" — reading R22: the standard closed-form
+ * Black-Scholes price of European options without dividends, with strike K, rate r,
+ * volatility v and maturity T fixed (the paper maps over the stock prices s only):
+ *     d1 = (ln(s/K) + (r + v^2/2) T) / (v sqrt(T)),   d2 = d1 - v sqrt(T)
+ *     call = s N(d1) - K e^{-rT} N(d2),   put = K e^{-rT} N(-d2) - s N(-d1)
+ *     N(x) = erfc(-x / sqrt(2)) / 2            (standard normal CDF)
+ * fp64 with the C library's erfc/log/exp/sqrt.  Pins: textbook values, put-call
+ * parity, the v -> 0 and s -> 0 limits (tests/test_oracle_bs.py). */
+static inline double norm_cdf(double x) { return 0.5 * erfc(-x / sqrt(2.0)); }
+
+void oracle_blackscholes(int64_t n, const float *s, double K, double r, double v, double T,
+                         double *call, double *put) {
+    const double vsqrt = v * sqrt(T);
+    const double disc = K * exp(-r * T);
+    for (int64_t i = 0; i < n; ++i) {
+        const double S = (double)s[i];
+        const double d1 = (log(S / K) + (r + 0.5 * v * v) * T) / vsqrt;  /* compD1 */
+        const double d2 = d1 - vsqrt;                                    /* compD2 */
+        call[i] = S * norm_cdf(d1) - disc * norm_cdf(d2);                /* compCall */
+        put[i] = disc * norm_cdf(-d2) - S * norm_cdf(-d1);               /* compPut */
+    }
+}

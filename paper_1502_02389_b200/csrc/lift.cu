@@ -210,41 +210,36 @@ const void* scal_fn(bool alias) {
     return alias ? (const void*)scal_kernel<LW, true> : (const void*)scal_kernel<LW, false>;
 }
 
-lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
-    a.cw = gemv_chunk_width(a.n);
-    a.nchunks = (int)((a.n + a.cw - 1) / a.cw);
-    const uintptr_t aa = reinterpret_cast<uintptr_t>(a.A);
-    const bool vec4 = (aa & 15) == 0 && a.lda % 4 == 0;
-    const bool tma_ok = vec4 && a.n >= 4 && a.n % 4 == 0 && a.n <= GEMV_NMAX_TMA &&
-                        (reinterpret_cast<uintptr_t>(a.x) & 15) == 0;
-    if (tma_ok) {
-        a.xs_stride = (int)((a.n + 3) / 4) + 1;
-        const size_t fixed = GEMV_CTRL_BYTES + gemv_xs_bytes(a.xs_stride);
-        int stages = (int)((GEMV_SMEM_LIMIT - fixed) / gemv_stage_bytes(a.cw));
-        if (stages > GEMV_SMAX) stages = GEMV_SMAX;
-        // x is staged through the ring before streaming starts: it must fit there
-        if (stages >= 2 && (size_t)stages * gemv_stage_bytes(a.cw) >= (size_t)a.n * 4) {
-            a.stages = stages;
-            const size_t smem = fixed + (size_t)stages * gemv_stage_bytes(a.cw);
-            const void* fn = (const void*)gemv_tma_kernel;
-            const int64_t units = (a.m + GEMV_RU - 1) / GEMV_RU;
-            const int64_t grid = grid_for(units, fn, (GEMV_WARPS + 1) * 32, smem, false, true);
-            gemv_tma_kernel<<<(unsigned)grid, (GEMV_WARPS + 1) * 32, smem, s>>>(a);
-            return launched();
-        }
-    }
-    a.xs_stride = 0;
-    a.stages = 0;
-    if (vec4) {
-        const int64_t grid = grid_for(a.m, (const void*)gemv_ldg_kernel<4>, GEMV_WARPS * 32, 0,
-                                      false, true);
-        gemv_ldg_kernel<4><<<(unsigned)grid, GEMV_WARPS * 32, 0, s>>>(a);
-    } else {
-        const int64_t grid = grid_for(a.m, (const void*)gemv_ldg_kernel<1>, GEMV_WARPS * 32, 0,
-                                      false, true);
-        gemv_ldg_kernel<1><<<(unsigned)grid, GEMV_WARPS * 32, 0, s>>>(a);
-    }
+template <int NT, int LW, bool MULTI>
+lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
+    const size_t smem = gemv_smem_bytes(a.P);
+    const void* fn = (const void*)gemv_kernel<NT, GEMV_R, GEMV_U, LW, MULTI>;
+    const int64_t rows_per_cta = (int64_t)(NT / 32) * GEMV_R;
+    const int64_t blocks = (a.m + rows_per_cta - 1) / rows_per_cta;
+    const int64_t grid = grid_for(blocks, fn, NT, smem, false, true);  // CLC steals the rest
+    gemv_kernel<NT, GEMV_R, GEMV_U, LW, MULTI><<<(unsigned)grid, NT, smem, s>>>(a);
     return launched();
+}
+
+template <int NT>
+lift_status gemv_pick(const GemvArgs& a, int lw, bool multi, cudaStream_t s) {
+    if (multi)
+        return lw == 8 ? gemv_go<NT, 8, true>(a, s) : lw == 4 ? gemv_go<NT, 4, true>(a, s)
+                                                             : gemv_go<NT, 1, true>(a, s);
+    return lw == 8 ? gemv_go<NT, 8, false>(a, s) : lw == 4 ? gemv_go<NT, 4, false>(a, s)
+                                                          : gemv_go<NT, 1, false>(a, s);
+}
+
+lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
+    const bool multi = a.n > GEMV_PMAX;
+    a.P = multi ? GEMV_PMAX : (int)(((a.n > 0 ? a.n : 1) + 255) / 256 * 256);
+    a.xs_stride = a.P / 8 + 1;
+    const uintptr_t aa = reinterpret_cast<uintptr_t>(a.A);
+    const int lw = ((aa & 31) == 0 && a.lda % 8 == 0) ? 8 : ((aa & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
+    // Two 256-thread CTAs per SM while x fits twice in shared memory; otherwise one
+    // 512-thread CTA, so an SM always runs 16 warps.
+    if (2 * gemv_smem_bytes(a.P) <= (size_t)GEMV_SMEM_LIMIT) return gemv_pick<256>(a, lw, multi, s);
+    return gemv_pick<512>(a, lw, multi, s);
 }
 
 }  // namespace

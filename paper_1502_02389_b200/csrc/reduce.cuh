@@ -53,6 +53,7 @@ struct AsumOp {
     template <class A2>
     using rebind = AsumOp<A2>;
     static constexpr bool kTwoInputs = false;
+    static constexpr int kMinBlocks = 6;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float) {
         if constexpr (sizeof(Acc) == 8) return __dadd_rn(acc, fabs((double)a));
         else return __fadd_rn(acc, fabsf(a));  // abs then add, fused
@@ -64,6 +65,7 @@ struct DotOp {
     template <class A2>
     using rebind = DotOp<A2>;
     static constexpr bool kTwoInputs = true;
+    static constexpr int kMinBlocks = 4;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float b) {
         if constexpr (sizeof(Acc) == 8) return __fma_rn((double)a, (double)b, acc);  // exact product
         else return __fmaf_rn(a, b, acc);  // mult then add, one rounding
@@ -149,8 +151,11 @@ __device__ __forceinline__ void chunk_body_tail(const float* xc, const float* yc
     }
 }
 
+// Resident CTAs per SM the register budget must allow (ptxas trades registers for how
+// many loads it issues up front).  Measured: asum 6 (all 4 loads up front, 40 regs),
+// dot 4 (all 8 loads up front); minBlocks 1 collapses occupancy (-40%).
 template <class Op, int LW, int B>
-__global__ void __launch_bounds__(RED_T) reduce_kernel(ReduceArgs a) {
+__global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     int parity = 0;
