@@ -127,6 +127,16 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
                       const float* x, float beta, const float* y, float* y_out,
                       lift_stream_t stream);
 
+/* NEXT-3 — BlackScholes (Fig. 9): map(BSComputation, s) over n stock prices.
+ *   call[i] = s_i N(d1) - K e^{-rT} N(d2),  put[i] = K e^{-rT} N(-d2) - s_i N(-d1),
+ *   d1 = (ln(s_i/K) + (r + v^2/2) T) / (v sqrt T),  d2 = d1 - v sqrt T,  N = normal CDF
+ *   (closed form; the paper does not print the helpers, P:825 — DESIGN.md reading R22).
+ *   s: n floats in (prices > 0); call, put: n floats out (SoA).  fp32 arithmetic with
+ *   IEEE-accurate logf/expf/erfcf (no fast math).  K, v, T must be > 0 and finite, r
+ *   finite, else LIFT_ERR_INVALID_VALUE.  n == 0 launches nothing. */
+lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,
+                              float* call, float* put, lift_stream_t stream);
+
 /* TEST HOOK: cap the number of CTAs any subsequent launch may use (0 = no cap,
  *   the default).  Used by the determinism tests to show results do not depend on
  *   the grid.  Process-global; not for production use. */

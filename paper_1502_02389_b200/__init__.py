@@ -21,7 +21,7 @@ import torch
 
 from ._lib import LiftError, check, lib
 
-__all__ = ["scal", "asum", "dot", "gemv", "asum_partial", "dot_partial", "combine",
+__all__ = ["scal", "asum", "dot", "gemv", "asum_partial", "dot_partial", "combine", "blackscholes",
            "workspace_bytes", "Workspace", "LiftError", "set_grid_limit"]
 
 
@@ -189,3 +189,14 @@ def gemv(A: torch.Tensor, x: torch.Tensor, y: torch.Tensor, alpha: float, beta: 
     check(lib.lift_gemv(m, n, float(alpha), A.data_ptr(), lda, x.data_ptr(), float(beta),
                         y.data_ptr(), yo.data_ptr(), _stream_handle(A.device)))
     return yo
+
+
+def blackscholes(s: torch.Tensor, K: float, r: float, v: float, T: float,
+                 call: torch.Tensor | None = None, put: torch.Tensor | None = None):
+    """(call, put) = map(BSComputation, s) (lift_blackscholes; Fig. 9)."""
+    s = _vec(s, "s")
+    c = _out(call, s.numel(), torch.float32, s.device, "call")
+    p = _out(put, s.numel(), torch.float32, s.device, "put")
+    check(lib.lift_blackscholes(s.numel(), s.data_ptr(), float(K), float(r), float(v), float(T),
+                                c.data_ptr(), p.data_ptr(), _stream_handle(s.device)))
+    return c, p

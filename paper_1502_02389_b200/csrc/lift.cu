@@ -11,6 +11,7 @@
 #include "../../include/lift.h"
 #include "canon.h"
 #include "common.cuh"
+#include "blackscholes.cuh"
 #include "gemv.cuh"
 #include "reduce.cuh"
 #include "scal.cuh"
@@ -357,6 +358,39 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
     a.y = y;
     a.y_out = y_out;
     return gemv_launch(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,
+                              float* call, float* put, lift_stream_t stream) {
+    if (n < 0) return LIFT_ERR_INVALID_VALUE;
+    if (!(K > 0.f) || !(v > 0.f) || !(T > 0.f) || !isfinite(r) || !isfinite(K) ||
+        !isfinite(v) || !isfinite(T))
+        return LIFT_ERR_INVALID_VALUE;
+    if (n == 0) return LIFT_OK;
+    if (!s || !call || !put) return LIFT_ERR_NULL_POINTER;
+    if (misaligned4(s) || misaligned4(call) || misaligned4(put)) return LIFT_ERR_INVALID_VALUE;
+    const uintptr_t as = reinterpret_cast<uintptr_t>(s), ac = reinterpret_cast<uintptr_t>(call),
+                    ap = reinterpret_cast<uintptr_t>(put);
+    // vector path needs s, call and put in the same 32-byte phase (then a common head)
+    const bool same = ((as - ac) & 31) == 0 && ((as - ap) & 31) == 0;
+    int64_t head = same ? (int64_t)(((32 - (as & 31)) & 31) / 4) : 0;
+    if (head > n) head = n;
+    const int64_t body = n - head;
+    const int64_t nslots = body / 8;
+    const int tail = (int)(body % 8);
+    const BsParams p{K, r, v, T};
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t tile = (int64_t)BS_T * BS_U;
+    if (same) {
+        const int64_t grid = grid_for((nslots + tile - 1) / tile, (const void*)blackscholes_kernel<8>,
+                                      BS_T, 0, false);
+        blackscholes_kernel<8><<<(unsigned)grid, BS_T, 0, st>>>(nslots, (int)head, tail, s, call, put, p);
+    } else {
+        const int64_t grid = grid_for((nslots + tile - 1) / tile, (const void*)blackscholes_kernel<1>,
+                                      BS_T, 0, false);
+        blackscholes_kernel<1><<<(unsigned)grid, BS_T, 0, st>>>(nslots, (int)head, tail, s, call, put, p);
+    }
+    return launched();
 }
 
 }  // extern "C"

@@ -104,6 +104,12 @@ def test_argument_errors_are_synchronous():
     assert lib.lift_gemv(0, 4, 1.0, None, 4, None, 1.0, None, None, None) == OK
     assert lib.lift_gemv(4, 4, 1.0, None, 4, p, 1.0, p, p, None) == NULLP
     assert lib.lift_gemv(4, 0, 1.0, None, 1, None, 1.0, None, p, None) == NULLP
+    assert lib.lift_blackscholes(-1, p, 100.0, 0.05, 0.2, 1.0, p, p, None) == INVALID
+    assert lib.lift_blackscholes(8, p, 0.0, 0.05, 0.2, 1.0, p, p, None) == INVALID   # K <= 0
+    assert lib.lift_blackscholes(8, p, 100.0, 0.05, -0.2, 1.0, p, p, None) == INVALID
+    assert lib.lift_blackscholes(8, p, 100.0, float("nan"), 0.2, 1.0, p, p, None) == INVALID
+    assert lib.lift_blackscholes(8, None, 100.0, 0.05, 0.2, 1.0, p, p, None) == NULLP
+    assert lib.lift_blackscholes(0, None, 100.0, 0.05, 0.2, 1.0, None, None, None) == OK
     assert lib.lift_debug_set_grid_limit(-1) == INVALID
     assert lib.lift_debug_set_grid_limit(0) == OK
 
