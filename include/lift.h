@@ -109,6 +109,14 @@ lift_status lift_asum_partial(int64_t n, const float* x, double* partial, void* 
 lift_status lift_dot_partial(int64_t n, const float* x, const float* y, double* partial,
                              void* ws, size_t ws_bytes, lift_stream_t stream);
 
+/* NEXT-2 — fused scal + asum (rule 5f across ops): in ONE pass over x,
+ *   y[i] = RN_fp32(alpha * x[i]) and *result = asum(y) — bit-identical to lift_scal
+ *   followed by lift_asum on y (same canonical fold of the same values), but x is read
+ *   once and y is not read back: 8 instead of 12 bytes per element.  y must not
+ *   overlap x (x == y -> LIFT_ERR_INVALID_VALUE).  Workspace as for lift_asum. */
+lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, float* result,
+                           void* ws, size_t ws_bytes, lift_stream_t stream);
+
 /* X1 — combine: *result = RN_fp32(pairwise_sum(partials[0..p))), the outermost
  *   reduce over per-rank partials in a fixed pairwise order (zero-padded to a power
  *   of two), so every rank that calls it on the gathered partials gets the same bits.

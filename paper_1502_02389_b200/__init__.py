@@ -22,6 +22,7 @@ import torch
 from ._lib import LiftError, check, lib
 
 __all__ = ["scal", "asum", "dot", "gemv", "asum_partial", "dot_partial", "combine", "blackscholes",
+           "scal_asum",
            "workspace_bytes", "Workspace", "LiftError", "set_grid_limit"]
 
 
@@ -131,6 +132,19 @@ def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None,
     check(lib.lift_dot(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
                        _stream_handle(x.device)))
     return r
+
+
+def scal_asum(alpha: float, x: torch.Tensor, out: torch.Tensor | None = None,
+              result: torch.Tensor | None = None, ws: Workspace | None = None):
+    """Fused y = alpha*x and asum(y) in one pass (lift_scal_asum).  Returns (y, result);
+    bit-identical to (scal(alpha, x), asum(scal(alpha, x))).  ``out`` must not be ``x``."""
+    x = _vec(x, "x")
+    y = _out(out, x.numel(), torch.float32, x.device)
+    r = _out(result, 1, torch.float32, x.device, "result")
+    w = ws or _workspace(x.numel(), x.device)
+    check(lib.lift_scal_asum(x.numel(), float(alpha), x.data_ptr(), y.data_ptr(), r.data_ptr(),
+                             w.ptr, w.nbytes, _stream_handle(x.device)))
+    return y, r
 
 
 def asum_partial(x: torch.Tensor, out: torch.Tensor | None = None,

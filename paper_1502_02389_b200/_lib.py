@@ -16,7 +16,7 @@ EXPORTS = (
     "lift_abi_version", "lift_status_string", "lift_workspace_bytes", "lift_scal",
     "lift_asum", "lift_dot", "lift_asum_partial", "lift_dot_partial", "lift_combine",
     "lift_gemv", "lift_debug_set_grid_limit", "lift_reduce_chunk_elems",
-    "lift_reduce_group_chunks", "lift_blackscholes",
+    "lift_reduce_group_chunks", "lift_blackscholes", "lift_scal_asum",
 )
 
 LIFT_OK = 0
@@ -46,6 +46,7 @@ def _load():
         "lift_debug_set_grid_limit": ([_int], _int),
         "lift_reduce_chunk_elems": ([], _i64),
         "lift_reduce_group_chunks": ([], _int),
+        "lift_scal_asum": ([_i64, _f32, _vp, _vp, _vp, _vp, _sz, _vp], _int),
         "lift_blackscholes": ([_i64, _vp, _f32, _f32, _f32, _f32, _vp, _vp, _vp], _int),
     }
     for name, (args, res) in sig.items():

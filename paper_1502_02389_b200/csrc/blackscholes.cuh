@@ -12,8 +12,10 @@
 //     call = s N(d1) - K e^{-rT} N(d2),   put = K e^{-rT} N(-d2) - s N(-d1)
 //     N(x) = erfc(-x/sqrt 2) / 2
 // fp32 storage and arithmetic (the paper's 4-byte elements) with the IEEE-
-// accurate libdevice logf/expf/erfcf/sqrtf (no fast math).  N(d) and N(-d) each come
-// from their own erfcf, so neither tail loses accuracy to 1 - N cancellation.
+// accurate libdevice logf/expf/erfcf/sqrtf (no fast math).  One erfcf per d: with
+// e = erfc(|d|/sqrt 2) (the small tail, relatively accurate), N(-|d|) = e/2 and
+// N(|d|) = 1 - e/2 (>= 1/2, so 1 - e/2 loses nothing) — both tails stay accurate
+// with half the erfcf calls of evaluating N(d) and N(-d) separately.
 //
 // B200 mapping: like scal — one CTA per tile, 8 consecutive prices per thread from
 // one 256-bit load, two 256-bit stores (call, put); the per-price transcendental
@@ -33,13 +35,13 @@ struct BsParams {
 };
 
 struct BsConst {
-    float logK, drift_T, vsqrt, inv_vsqrt, disc;
+    float invK, drift_T, vsqrt, inv_vsqrt, disc;
 };
 
 __device__ __forceinline__ BsConst bs_const(const BsParams& p) {
     BsConst c;
     const float sqrtT = sqrtf(p.T);
-    c.logK = logf(p.K);
+    c.invK = 1.0f / p.K;
     c.drift_T = (p.r + 0.5f * p.v * p.v) * p.T;
     c.vsqrt = p.v * sqrtT;
     c.inv_vsqrt = 1.0f / c.vsqrt;
@@ -47,16 +49,23 @@ __device__ __forceinline__ BsConst bs_const(const BsParams& p) {
     return c;
 }
 
+// N(d) and N(-d) from a single erfcf (see the header comment).
+__device__ __forceinline__ void norm_cdf_pair(float d, float& n_pos, float& n_neg) {
+    constexpr float kRsqrt2 = 0.70710678118654752440f;
+    const float half_tail = 0.5f * erfcf(fabsf(d) * kRsqrt2);  // N(-|d|)
+    const float body = 1.0f - half_tail;                        // N(|d|)
+    n_pos = d >= 0.f ? body : half_tail;                        // N(d)
+    n_neg = d >= 0.f ? half_tail : body;                        // N(-d)
+}
+
 // One BSComputation.
 __device__ __forceinline__ void bs_one(float S, const BsConst& c, const BsParams& p, float& call,
                                        float& put) {
-    const float d1 = (logf(S / p.K) + c.drift_T) * c.inv_vsqrt;  // compD1
-    const float d2 = d1 - c.vsqrt;                               // compD2
-    constexpr float kRsqrt2 = 0.70710678118654752440f;
-    const float n_d1 = 0.5f * erfcf(-d1 * kRsqrt2);
-    const float n_d2 = 0.5f * erfcf(-d2 * kRsqrt2);
-    const float n_md1 = 0.5f * erfcf(d1 * kRsqrt2);
-    const float n_md2 = 0.5f * erfcf(d2 * kRsqrt2);
+    const float d1 = (logf(S * c.invK) + c.drift_T) * c.inv_vsqrt;  // compD1
+    const float d2 = d1 - c.vsqrt;                                  // compD2
+    float n_d1, n_md1, n_d2, n_md2;
+    norm_cdf_pair(d1, n_d1, n_md1);
+    norm_cdf_pair(d2, n_d2, n_md2);
     call = __fmaf_rn(S, n_d1, -c.disc * n_d2);   // compCall
     put = __fmaf_rn(c.disc, n_md2, -S * n_md1);  // compPut
 }

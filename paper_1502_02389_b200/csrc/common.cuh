@@ -68,6 +68,20 @@ __device__ __forceinline__ f8 ld_slot(const float* p) {
     }
 }
 
+// Store one 8-float slot with the widest access the alignment class allows.
+template <int LW>
+__device__ __forceinline__ void st_slot(float* p, const f8& v) {
+    if constexpr (LW == 8) {
+        st_v8(p, v);
+    } else if constexpr (LW == 4) {
+        reinterpret_cast<float4*>(p)[0] = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
+        reinterpret_cast<float4*>(p)[1] = make_float4(v.v[4], v.v[5], v.v[6], v.v[7]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p[e] = v.v[e];
+    }
+}
+
 // Fixed pairwise fold of 8 fp64 values: ((v0+v1)+(v2+v3))+((v4+v5)+(v6+v7)).
 __device__ __forceinline__ double pairwise8(const double* v) {
     return __dadd_rn(__dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])),

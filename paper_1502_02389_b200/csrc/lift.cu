@@ -157,14 +157,17 @@ size_t ws_bytes_for(int64_t n) {
 
 template <class Op, int B>
 lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out32, double* out64,
-                          void* ws, size_t ws_bytes, cudaStream_t stream) {
+                          void* ws, size_t ws_bytes, cudaStream_t stream, float alpha = 0.f,
+                          float* map_out = nullptr) {
     if (n < 0) return LIFT_ERR_INVALID_VALUE;
     if (!out32 && !out64) return LIFT_ERR_NULL_POINTER;
-    if (n > 0 && (!x || (Op::kTwoInputs && !y) || !ws)) return LIFT_ERR_NULL_POINTER;
+    if (n > 0 && (!x || (Op::kTwoInputs && !y) || !ws || (Op::kMapStore && !map_out)))
+        return LIFT_ERR_NULL_POINTER;
+    if (Op::kMapStore && misaligned4(map_out)) return LIFT_ERR_INVALID_VALUE;
     if (misaligned4(x) || (Op::kTwoInputs && misaligned4(y)) || misaligned4(out32) ||
         (reinterpret_cast<uintptr_t>(out64) & 7))
         return LIFT_ERR_INVALID_VALUE;
-    if (n == 0) {  // reduce over an empty array yields z = +0
+    if (n == 0) {  // reduce over an empty array yields z = +0; no map
         if (out32 && cudaMemsetAsync(out32, 0, sizeof(float), stream) != cudaSuccess)
             return LIFT_ERR_CUDA;
         if (out64 && cudaMemsetAsync(out64, 0, sizeof(double), stream) != cudaSuccess)
@@ -186,9 +189,12 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     a.group_part = a.chunk_part + L.nc;
     a.out_f32 = out32;
     a.out_f64 = out64;
+    a.alpha = alpha;
+    a.map_out = map_out;
 
     uintptr_t al = reinterpret_cast<uintptr_t>(x);
     if (Op::kTwoInputs) al |= reinterpret_cast<uintptr_t>(y);
+    if (Op::kMapStore) al |= reinterpret_cast<uintptr_t>(map_out);
     const int lw = align_class(al);
     const void* fn = lw == 8 ? (const void*)reduce_kernel<Op, 8, B>
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
@@ -327,6 +333,15 @@ lift_status lift_dot_partial(int64_t n, const float* x, const float* y, double* 
     if (!partial) return LIFT_ERR_NULL_POINTER;
     return reduce_launch<DotOp<LIFT_DOT_ACC>, LIFT_DOT_B>(n, x, y, nullptr, partial, ws, ws_bytes,
                                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, float* result,
+                           void* ws, size_t ws_bytes, lift_stream_t stream) {
+    if (!result) return LIFT_ERR_NULL_POINTER;
+    if (n > 0 && x && y && x == y) return LIFT_ERR_INVALID_VALUE;  // x is read on the .nc path
+    return reduce_launch<ScalAsumOp<LIFT_ASUM_ACC>, LIFT_ASUM_B>(
+        n, x, nullptr, result, nullptr, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), alpha,
+        y);
 }
 
 lift_status lift_combine(int p, const double* partials, float* result, lift_stream_t stream) {

@@ -53,6 +53,7 @@ struct AsumOp {
     template <class A2>
     using rebind = AsumOp<A2>;
     static constexpr bool kTwoInputs = false;
+    static constexpr bool kMapStore = false;
     static constexpr int kMinBlocks = 6;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float) {
         if constexpr (sizeof(Acc) == 8) return __dadd_rn(acc, fabs((double)a));
@@ -65,10 +66,31 @@ struct DotOp {
     template <class A2>
     using rebind = DotOp<A2>;
     static constexpr bool kTwoInputs = true;
+    static constexpr bool kMapStore = false;
     static constexpr int kMinBlocks = 4;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float b) {
         if constexpr (sizeof(Acc) == 8) return __fma_rn((double)a, (double)b, acc);  // exact product
         else return __fmaf_rn(a, b, acc);  // mult then add, one rounding
+    }
+};
+
+// NEXT-2 — cross-op fusion by rule 5f: asum(scal(a, x)).
+//   map(f) o map(g) -> map(f o g) and reduce-seq(f) o map-seq(g) -> one fold, so
+//   y = scal(a, x) is written AND asum(y) is folded in the same pass over x: 8 bytes
+//   per element instead of scal's 8 plus asum's 4.  The fold consumes exactly the
+//   stored y values in asum's canonical order, so the result is bit-identical to
+//   lift_asum(lift_scal(x)).
+template <class Acc>
+struct ScalAsumOp {
+    using acc_t = Acc;
+    template <class A2>
+    using rebind = ScalAsumOp<A2>;
+    static constexpr bool kTwoInputs = false;
+    static constexpr bool kMapStore = true;
+    static constexpr int kMinBlocks = 4;
+    __device__ __forceinline__ static float map(float a, float alpha) { return __fmul_rn(alpha, a); }
+    __device__ __forceinline__ static Acc step(Acc acc, float m, float) {
+        return AsumOp<Acc>::step(acc, m, 0.f);
     }
 };
 
@@ -83,6 +105,8 @@ struct ReduceArgs {
     double* group_part;  // ng
     float* out_f32;      // may be null
     double* out_f64;     // may be null
+    float alpha;         // kMapStore ops: the map's scalar
+    float* map_out;      // kMapStore ops: where the mapped values are stored (n floats)
 };
 
 // Warp-level pairwise fold of `nleaf` fp64 leaves read from global memory (L2),
@@ -114,7 +138,8 @@ __device__ __forceinline__ double warp_fold_leaves(const double* leaves, int64_t
 
 template <class Op, int LW, int B0>
 __device__ __forceinline__ void chunk_body_full(const float* xc, const float* yc,
-                                                typename Op::acc_t* acc) {
+                                                typename Op::acc_t* acc, float alpha = 0.f,
+                                                float* mo = nullptr) {
     constexpr int B = B0 < RED_K ? B0 : RED_K;
     static_assert(RED_K % B == 0, "load batch must divide RED_K");
     const int t = threadIdx.x;
@@ -128,6 +153,14 @@ __device__ __forceinline__ void chunk_body_full(const float* xc, const float* yc
             if constexpr (Op::kTwoInputs)
                 yv[b] = ld_slot<LW>(yc + (int64_t)RED_V * (t + (k0 + b) * RED_T));
         }
+        if constexpr (Op::kMapStore) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+#pragma unroll
+                for (int e = 0; e < RED_V; ++e) xv[b].v[e] = Op::map(xv[b].v[e], alpha);
+                st_slot<LW>(mo + (int64_t)RED_V * (t + (k0 + b) * RED_T), xv[b]);
+            }
+        }
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -140,13 +173,21 @@ __device__ __forceinline__ void chunk_body_full(const float* xc, const float* yc
 // +0 exactly (the accumulators start at +0 and can never become -0 in RN).
 template <class Op>
 __device__ __forceinline__ void chunk_body_tail(const float* xc, const float* yc, int64_t len,
-                                                typename Op::acc_t* acc) {
+                                                typename Op::acc_t* acc, float alpha = 0.f,
+                                                float* mo = nullptr) {
     const int t = threadIdx.x;
     for (int k = 0; k < RED_K; ++k) {
 #pragma unroll
         for (int e = 0; e < RED_V; ++e) {
             const int64_t j = (int64_t)RED_V * (t + k * RED_T) + e;
-            if (j < len) acc[e] = Op::step(acc[e], xc[j], Op::kTwoInputs ? yc[j] : 0.f);
+            if (j < len) {
+                float v = xc[j];
+                if constexpr (Op::kMapStore) {
+                    v = Op::map(v, alpha);
+                    mo[j] = v;
+                }
+                acc[e] = Op::step(acc[e], v, Op::kTwoInputs ? yc[j] : 0.f);
+            }
         }
     }
 }
@@ -169,8 +210,9 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
 #pragma unroll
         for (int e = 0; e < RED_V; ++e) acc[e] = 0;
         const bool full = base + RED_C <= a.n;
-        if (full) chunk_body_full<Op, LW, B>(xc, yc, acc);
-        else chunk_body_tail<Op>(xc, yc, a.n - base, acc);
+        float* mo = Op::kMapStore ? a.map_out + base : nullptr;
+        if (full) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo);
+        else chunk_body_tail<Op>(xc, yc, a.n - base, acc, a.alpha, mo);
 
         // ---- R3: lane -> warp (butterfly) -> CTA (8 warps pairwise), fp64 --------
         double lane8[RED_V];
@@ -187,12 +229,17 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
         else __syncthreads();
         if constexpr (sizeof(acc[0]) == 4) {
             if (redo) {  // rare: an fp32 run overflowed (or the chunk holds Inf/NaN)
-                using Op64 = typename Op::template rebind<double>;
                 double acc64[RED_V];
 #pragma unroll
                 for (int e = 0; e < RED_V; ++e) acc64[e] = 0.0;
-                if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64);
-                else chunk_body_tail<Op64>(xc, yc, a.n - base, acc64);
+                if constexpr (Op::kMapStore) {
+                    // refold this thread's own stored map values
+                    chunk_body_tail<AsumOp<double>>(mo, nullptr, min((int64_t)RED_C, a.n - base), acc64);
+                } else {
+                    using Op64 = typename Op::template rebind<double>;
+                    if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64);
+                    else chunk_body_tail<Op64>(xc, yc, a.n - base, acc64);
+                }
                 wv = warp_pairwise(pairwise8(acc64));
                 if (lane == 0) wbuf[parity][warp] = wv;  // nobody reads wbuf before the barrier
                 __syncthreads();

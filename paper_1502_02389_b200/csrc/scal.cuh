@@ -18,19 +18,6 @@ namespace lift {
 constexpr int SCAL_T = 256;  // threads per CTA
 constexpr int SCAL_U = 4;    // 8-float slots per thread per tile (4 x 32 B in flight)
 
-template <int LW>
-__device__ __forceinline__ void st_slot(float* p, const f8& v) {
-    if constexpr (LW == 8) {
-        st_v8(p, v);
-    } else if constexpr (LW == 4) {
-        reinterpret_cast<float4*>(p)[0] = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
-        reinterpret_cast<float4*>(p)[1] = make_float4(v.v[4], v.v[5], v.v[6], v.v[7]);
-    } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) p[e] = v.v[e];
-    }
-}
-
 template <int LW, bool ALIAS>
 __device__ __forceinline__ f8 scal_load(const float* p) {
     if constexpr (LW == 8 && ALIAS) return ld_v8(p);  // x == y: stay off the .nc path

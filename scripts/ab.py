@@ -33,6 +33,9 @@ def child(reps=30):
     go = torch.empty(8192, dtype=torch.float32, device=dev)
     r = torch.empty(1, dtype=torch.float32, device=dev)
     ws = lift.Workspace(1 << 28, dev)
+    bs_s = fill(4 << 20, 1, 10.0, 200.0)
+    bs_c = torch.empty(4 << 20, dtype=torch.float32, device=dev)
+    bs_p = torch.empty(4 << 20, dtype=torch.float32, device=dev)
     ops = {
         "scal_2p28": (lambda: lift.scal(3.0, x, out=y), 8 << 28),
         "asum_2p28": (lambda: lift.asum(x, out=r, ws=ws), 4 << 28),
@@ -41,6 +44,9 @@ def child(reps=30):
         "gemv_8192x16384": (lambda: lift.gemv(A2, gx2, gy, 1.5, 0.5, out=go),
                             4 * (8192 * 16384 + 16384 + 2 * 8192)),
         "asum_2p20": (lambda: lift.asum(x[:1 << 20], out=r, ws=ws), 4 << 20),
+        "scal_asum_2p28": (lambda: lift.scal_asum(3.0, x, out=y, result=r, ws=ws), 8 << 28),
+        "bs_4M": (lambda: lift.blackscholes(bs_s, 100.0, 0.05, 0.2, 1.0, call=bs_c, put=bs_p),
+                  12 * (4 << 20)),
     }
     out = {}
     samples = {name: [] for name in ops}

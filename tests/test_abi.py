@@ -110,6 +110,9 @@ def test_argument_errors_are_synchronous():
     assert lib.lift_blackscholes(8, p, 100.0, float("nan"), 0.2, 1.0, p, p, None) == INVALID
     assert lib.lift_blackscholes(8, None, 100.0, 0.05, 0.2, 1.0, p, p, None) == NULLP
     assert lib.lift_blackscholes(0, None, 100.0, 0.05, 0.2, 1.0, None, None, None) == OK
+    assert lib.lift_scal_asum(10, 2.0, p, p, p, p, 1 << 20, None) == INVALID     # y == x
+    assert lib.lift_scal_asum(10, 2.0, p, None, p, p, 1 << 20, None) == NULLP
+    assert lib.lift_scal_asum(10, 2.0, p, p + 64, None, p, 1 << 20, None) == NULLP
     assert lib.lift_debug_set_grid_limit(-1) == INVALID
     assert lib.lift_debug_set_grid_limit(0) == OK
 
