@@ -336,7 +336,7 @@ def run_lift(args):
             "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "accum": "f64 (exact products, fp64 lane folds and partials; fp32 storage)",
+            "dtype": "f32", "accum": "asum f32 4-term runs then f64; dot/gemv exact products in f64",
             "data": "synthetic (seeded counter-based generator, device-filled)",
             "config": {"workload": "step = scal+asum fp32 n=2^28 (configs[2]) + dot fp32 "
                                    "n=2^26 (configs[1]) + gemv 8192x8192 a=1.5 b=0.5 "

@@ -262,6 +262,14 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
         __threadfence();
         const int64_t g0 = g * RED_G;
         const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
+        if (a.ng == 1) {  // one group: the pairwise fold over one leaf is the leaf itself
+            if (lane == 0) {
+                if (a.out_f64) *a.out_f64 = gpart;
+                if (a.out_f32) *a.out_f32 = __double2float_rn(gpart);
+                a.tick[0] = 0u;
+            }
+            continue;
+        }
         last = 0;
         if (lane == 0) {
             a.group_part[g] = gpart;

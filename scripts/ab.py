@@ -1,8 +1,10 @@
 """A/B timing of liblift builds: python scripts/ab.py lib1.so [lib2.so ...]
 
 Each library (same ABI, different compile-time tuning) runs in its own subprocess
-(LIFT_LIB=...).  Per op: median of R event-timed launches, inputs > L2 (no reuse
-between launches: operands are >= 256 MiB).  Prints one JSON line per library."""
+(LIFT_LIB=...).  Per op: `reps` back-to-back launches captured in one CUDA graph
+(no Python launch overhead), median over 5 interleaved replays; operands >= 256 MiB
+exceed L2 except the small asum_2p20 case (L2-resident by design: latency).
+Prints one JSON line per library."""
 import json
 import os
 import subprocess
@@ -50,16 +52,24 @@ def child(reps=30):
     }
     out = {}
     samples = {name: [] for name in ops}
-    for name, (fn, _) in ops.items():
-        for _ in range(5):
-            fn()
+    graphs = {}
+    cs = torch.cuda.Stream(device=dev)
+    for name, (fn, _) in ops.items():  # warm, then capture `reps` launches per op
+        with torch.cuda.stream(cs):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs):
+                for _ in range(reps):
+                    fn()
+        graphs[name] = g
     torch.cuda.synchronize()
-    for _ in range(5):  # rounds interleaved across ops; each = `reps` back-to-back launches
-        for name, (fn, nbytes) in ops.items():
+    for _ in range(5):  # rounds interleaved across ops; each = one replay of `reps` launches
+        for name in ops:
             s, e = torch.cuda.Event(True), torch.cuda.Event(True)
             s.record()
-            for _ in range(reps):
-                fn()
+            graphs[name].replay()
             e.record()
             e.synchronize()
             samples[name].append(s.elapsed_time(e) / reps)
