@@ -1,0 +1,41 @@
+"""Small invocations of every kernel and launch path, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck):  compute-sanitizer --tool <t> python scripts/sanitize_probe.py"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_1502_02389_b200 as lift  # noqa: E402
+
+dev = torch.device("cuda:0")
+g = torch.Generator(device="cpu").manual_seed(0)
+
+
+def rnd(n, off=0):
+    buf = torch.empty(n + off + 8, device=dev)
+    v = buf[off:off + n]
+    v.copy_(torch.rand(n, generator=g) * 2 - 1)
+    return v
+
+
+C = lift.CHUNK_ELEMS
+for n, off in [(0, 0), (1, 0), (13, 3), (C + 5, 0), (C + 5, 1), (2 * lift.GROUP_ELEMS + 77, 4)]:
+    x, y = rnd(n, off), rnd(n, (off * 3) % 8)
+    lift.scal(3.0, x)
+    lift.scal(3.0, x, out=x)
+    lift.asum(x), lift.dot(x, y), lift.asum_partial(x), lift.dot_partial(x, y)
+    if n:
+        out = torch.empty(n + 8, device=dev)[1:1 + n] if off else None
+        lift.scal_asum(2.0, x, out=out)
+        lift.blackscholes(x.abs() + 1.0, 1.5, 0.05, 0.2, 1.0)
+lift.combine(torch.rand(5, dtype=torch.float64, device=dev))
+x = rnd(1000)
+x[7] = float("inf")
+lift.asum(x)  # fp64 refold path
+for m, n, pad in [(3, 5, 0), (40, 1000, 3), (40, 8192, 0), (17, 9000, 4), (5, 20000, 0)]:
+    A = torch.rand(m, n + pad, generator=g).to(dev)[:, :n]
+    lift.gemv(A, rnd(n), rnd(m), 1.5, 0.5)
+torch.cuda.synchronize()
+print("sanitize probe ok")
