@@ -207,10 +207,17 @@ def run_lift(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # LIFT_DIST_BACKEND=gloo (test only) runs N ranks on fewer GPUs: exercises the N>1
+    # code path on a single-GPU box; the performance numbers of such a run are meaningless.
+    backend = os.environ.get("LIFT_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     group = None
     stream = torch.cuda.current_stream(dev)
 
