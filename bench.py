@@ -194,6 +194,11 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------- lift arm
+def _dbg(msg):
+    if os.environ.get("LIFT_BENCH_DEBUG"):
+        print(f"[rank {os.environ.get('RANK', '0')}] {msg}", file=sys.stderr, flush=True)
+
+
 def run_lift(args):
     import torch
     import torch.distributed as dist
@@ -278,9 +283,11 @@ def run_lift(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    _dbg("inputs ready")
     for _ in range(max(args.warmup, 0)):
         step()
     barrier()
+    _dbg("warm-up done")
 
     # ---- timed region: K steps, per-op events on the launching stream ---------------
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
@@ -298,14 +305,20 @@ def run_lift(args):
     end.record(stream)
     barrier()
     t_wall1 = time.time()
-    # keep the GPU busy until the sampler has seen the load (short K on a fast GPU)
+    # keep the GPU busy until the sampler has seen the load (short K on a fast GPU).
+    # Untimed and rank-local: only the kernels, never the X1 collectives (rank 0 alone
+    # runs this loop, so a collective here would deadlock the other ranks).
     while sampler and len([1 for (t, _) in sampler.rows if t >= t_wall0]) < 5 \
             and time.time() - t_wall0 < 10:
-        step()
+        lift.scal(ALPHA_SCAL, x_v, out=y_v)
+        lift.asum(x_v, out=r_asum, ws=ws_a)
+        lift.dot(x_d, y_d, out=r_dot, ws=ws_d)
+        lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out)
         torch.cuda.synchronize()
     t_wall2 = time.time()
     if sampler:
         sampler.stop()
+    _dbg("timed region done")
     total_ms = max_over_ranks(start.elapsed_time(end))
     per_op_ms = {op: 0.0 for op in OPS}
     for k in range(args.steps):
@@ -320,6 +333,7 @@ def run_lift(args):
 
     # ---- e2e: the same step through the public API with pinned HOST buffers --------
     e2e = None
+    _dbg("per-op times reduced")
     if not args.no_e2e:
         e2e = run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
                       max_over_ranks, barrier, step_bytes)
