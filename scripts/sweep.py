@@ -65,6 +65,13 @@ for k in range(16, 29, 2):
     out[f"asum_2^{k}"] = time_op(lambda: lift.asum(xs, out=r, ws=ws), 4 * n)
     out[f"dot_2^{k}"] = time_op(lambda: lift.dot(xs, ys, out=r, ws=ws), 8 * n)
 del x, y, yo
+# C5: dot over 2^31 elements on one GPU (16 GiB of inputs), as one launch
+big_x = fill(1 << 31, 1, 0.0, 1.0)
+big_y = fill(1 << 31, 2, 0.0, 2.0)
+wsb = lift.Workspace(1 << 31, dev)
+out["dot_2^31"] = time_op(lambda: lift.dot(big_x, big_y, out=r, ws=wsb), 8 << 31, reps=5,
+                          flush_l2=False)
+del big_x, big_y
 for (m, n) in [(4096, 4096), (8192, 8192), (8192, 16384)]:
     A = fill(m * n, 3, 0.0, 3.0).view(m, n)
     gx, gy = fill(n, 1, 0.0, 1.0), fill(m, 2, 0.0, 2.0)
