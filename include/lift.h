@@ -117,6 +117,35 @@ lift_status lift_dot_partial(int64_t n, const float* x, const float* y, double* 
 lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, float* result,
                            void* ws, size_t ws_bytes, lift_stream_t stream);
 
+/* NEXT-1 — fused cross-GPU combine over peer memory (NVLink P2P stores).
+ *   Each rank owns an EXCHANGE BUFFER of lift_xchg_bytes(p) bytes (lift_xchg_create:
+ *   cudaMalloc'd and zeroed; the caller owns it and frees it with lift_xchg_destroy).
+ *   Ranks share buffers with CUDA IPC (lift_ipc_get_handle / lift_ipc_open_handle; the
+ *   64-byte handles travel over any host channel) and pass `peers`, a DEVICE array of p
+ *   device pointers with peers[rank] = the own buffer, the others IPC-mapped.
+ *   lift_*_allreduce run the single-pass reduction; its final CTA stores the fp64
+ *   partial into slot `rank` of every peer's buffer, raises the slot flag to `epoch`
+ *   (system-scope release), waits for all p flags of its own buffer and folds the p
+ *   partials pairwise in rank order: every rank gets the SAME fp32 bits, equal to
+ *   lift_combine over the gathered *_partial results — with no separate collective.
+ *   p in [1, 32]; epoch > 0 and strictly increasing per call on the same buffers (two
+ *   banks alternate by epoch parity); all p ranks must make the matching call.  The
+ *   wait is bounded (~2 s): on timeout *result = NaN and *error (device int, may be
+ *   NULL) is set to 1.  Workspace as for lift_asum. */
+#define LIFT_IPC_HANDLE_BYTES 64
+size_t lift_xchg_bytes(int p);
+lift_status lift_xchg_create(int p, void** buf);
+lift_status lift_xchg_destroy(void* buf);
+lift_status lift_ipc_get_handle(const void* buf, void* handle);
+lift_status lift_ipc_open_handle(const void* handle, void** ptr);
+lift_status lift_ipc_close_handle(void* ptr);
+lift_status lift_asum_allreduce(int64_t n, const float* x, float* result, void* ws,
+                                size_t ws_bytes, void* const* peers, int p, int rank,
+                                unsigned long long epoch, int* error, lift_stream_t stream);
+lift_status lift_dot_allreduce(int64_t n, const float* x, const float* y, float* result,
+                               void* ws, size_t ws_bytes, void* const* peers, int p, int rank,
+                               unsigned long long epoch, int* error, lift_stream_t stream);
+
 /* X1 — combine: *result = RN_fp32(pairwise_sum(partials[0..p))), the outermost
  *   reduce over per-rank partials in a fixed pairwise order (zero-padded to a power
  *   of two), so every rank that calls it on the gathered partials gets the same bits.

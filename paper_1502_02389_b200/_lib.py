@@ -16,7 +16,9 @@ EXPORTS = (
     "lift_abi_version", "lift_status_string", "lift_workspace_bytes", "lift_scal",
     "lift_asum", "lift_dot", "lift_asum_partial", "lift_dot_partial", "lift_combine",
     "lift_gemv", "lift_debug_set_grid_limit", "lift_reduce_chunk_elems",
-    "lift_reduce_group_chunks", "lift_blackscholes", "lift_scal_asum",
+    "lift_reduce_group_chunks", "lift_blackscholes", "lift_scal_asum", "lift_xchg_bytes",
+    "lift_xchg_create", "lift_xchg_destroy", "lift_ipc_get_handle", "lift_ipc_open_handle",
+    "lift_ipc_close_handle", "lift_asum_allreduce", "lift_dot_allreduce",
 )
 
 LIFT_OK = 0
@@ -47,6 +49,16 @@ def _load():
         "lift_reduce_chunk_elems": ([], _i64),
         "lift_reduce_group_chunks": ([], _int),
         "lift_scal_asum": ([_i64, _f32, _vp, _vp, _vp, _vp, _sz, _vp], _int),
+        "lift_xchg_bytes": ([_int], _sz),
+        "lift_xchg_create": ([_int, ctypes.POINTER(ctypes.c_void_p)], _int),
+        "lift_xchg_destroy": ([_vp], _int),
+        "lift_ipc_get_handle": ([_vp, _vp], _int),
+        "lift_ipc_open_handle": ([_vp, ctypes.POINTER(ctypes.c_void_p)], _int),
+        "lift_ipc_close_handle": ([_vp], _int),
+        "lift_asum_allreduce": ([_i64, _vp, _vp, _vp, _sz, _vp, _int, _int, ctypes.c_ulonglong,
+                                 _vp, _vp], _int),
+        "lift_dot_allreduce": ([_i64, _vp, _vp, _vp, _vp, _sz, _vp, _int, _int,
+                                ctypes.c_ulonglong, _vp, _vp], _int),
         "lift_blackscholes": ([_i64, _vp, _f32, _f32, _f32, _f32, _vp, _vp, _vp], _int),
     }
     for name, (args, res) in sig.items():

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 
 #include "../../include/lift.h"
@@ -50,10 +51,7 @@ namespace {
 
 std::atomic<int> g_grid_limit{0};
 
-struct DevInfo {
-    int sms = 0;
-};
-DevInfo g_dev[64];
+std::atomic<int> g_sms[64];  // per-device SM count cache (0 = not yet queried)
 std::mutex g_mu;
 
 struct OccEntry {
@@ -73,12 +71,13 @@ int current_device() {
 
 int sm_count(int dev) {
     if (dev < 0 || dev >= 64) return 148;
-    if (g_dev[dev].sms == 0) {
-        int s = 0;
+    int s = g_sms[dev].load(std::memory_order_relaxed);
+    if (s == 0) {
         cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-        g_dev[dev].sms = s > 0 ? s : 148;
+        if (s <= 0) s = 148;
+        g_sms[dev].store(s, std::memory_order_relaxed);
     }
-    return g_dev[dev].sms;
+    return s;
 }
 
 // Resident CTAs per SM for `fn` (cached).  Also raises the dynamic smem limit.
@@ -155,10 +154,17 @@ size_t ws_bytes_for(int64_t n) {
     return w;
 }
 
+struct XchgArgs {  // NEXT-1: in-kernel cross-GPU combine (all null: single GPU)
+    void* const* peers = nullptr;
+    int p = 1, rank = 0;
+    unsigned long long epoch = 0;
+    int* error = nullptr;
+};
+
 template <class Op, int B>
 lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out32, double* out64,
                           void* ws, size_t ws_bytes, cudaStream_t stream, float alpha = 0.f,
-                          float* map_out = nullptr) {
+                          float* map_out = nullptr, const XchgArgs& xa = XchgArgs()) {
     if (n < 0) return LIFT_ERR_INVALID_VALUE;
     if (!out32 && !out64) return LIFT_ERR_NULL_POINTER;
     if (n > 0 && (!x || (Op::kTwoInputs && !y) || !ws || (Op::kMapStore && !map_out)))
@@ -167,6 +173,18 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     if (misaligned4(x) || (Op::kTwoInputs && misaligned4(y)) || misaligned4(out32) ||
         (reinterpret_cast<uintptr_t>(out64) & 7))
         return LIFT_ERR_INVALID_VALUE;
+    if (n == 0 && xa.peers) {  // still publish (+0) and combine with the other ranks
+        ReduceArgs a{};
+        a.out_f32 = out32;
+        a.out_f64 = out64;
+        a.peers = xa.peers;
+        a.p = xa.p;
+        a.rank = xa.rank;
+        a.epoch = xa.epoch;
+        a.error = xa.error;
+        xchg_only_kernel<<<1, 32, 0, stream>>>(a);
+        return launched();
+    }
     if (n == 0) {  // reduce over an empty array yields z = +0; no map
         if (out32 && cudaMemsetAsync(out32, 0, sizeof(float), stream) != cudaSuccess)
             return LIFT_ERR_CUDA;
@@ -191,6 +209,11 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     a.out_f64 = out64;
     a.alpha = alpha;
     a.map_out = map_out;
+    a.peers = xa.peers;
+    a.p = xa.p;
+    a.rank = xa.rank;
+    a.epoch = xa.epoch;
+    a.error = xa.error;
 
     uintptr_t al = reinterpret_cast<uintptr_t>(x);
     if (Op::kTwoInputs) al |= reinterpret_cast<uintptr_t>(y);
@@ -342,6 +365,85 @@ lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, flo
     return reduce_launch<ScalAsumOp<LIFT_ASUM_ACC>, LIFT_ASUM_B>(
         n, x, nullptr, result, nullptr, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), alpha,
         y);
+}
+
+size_t lift_xchg_bytes(int p) { return p < 1 ? 0 : (size_t)2 * p * sizeof(XchgSlot); }
+
+lift_status lift_xchg_create(int p, void** buf) {
+    if (p < 1 || p > 32) return LIFT_ERR_INVALID_VALUE;
+    if (!buf) return LIFT_ERR_NULL_POINTER;
+    void* d = nullptr;
+    if (cudaMalloc(&d, lift_xchg_bytes(p)) != cudaSuccess) return LIFT_ERR_CUDA;
+    if (cudaMemset(d, 0, lift_xchg_bytes(p)) != cudaSuccess) {
+        cudaFree(d);
+        return LIFT_ERR_CUDA;
+    }
+    *buf = d;
+    return LIFT_OK;
+}
+
+lift_status lift_xchg_destroy(void* buf) {
+    if (!buf) return LIFT_OK;
+    return cudaFree(buf) == cudaSuccess ? LIFT_OK : LIFT_ERR_CUDA;
+}
+
+lift_status lift_ipc_get_handle(const void* buf, void* handle) {
+    if (!buf || !handle) return LIFT_ERR_NULL_POINTER;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, const_cast<void*>(buf)) != cudaSuccess) return LIFT_ERR_CUDA;
+    static_assert(sizeof(h) == LIFT_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+    return LIFT_OK;
+}
+
+lift_status lift_ipc_open_handle(const void* handle, void** ptr) {
+    if (!handle || !ptr) return LIFT_ERR_NULL_POINTER;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    if (cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return LIFT_ERR_CUDA;
+    return LIFT_OK;
+}
+
+lift_status lift_ipc_close_handle(void* ptr) {
+    if (!ptr) return LIFT_OK;
+    return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? LIFT_OK : LIFT_ERR_CUDA;
+}
+
+static lift_status xchg_check(void* const* peers, int p, int rank, unsigned long long epoch,
+                              XchgArgs& xa, int* error) {
+    if (p < 1 || p > 32 || rank < 0 || rank >= p || epoch == 0) return LIFT_ERR_INVALID_VALUE;
+    if (!peers) return LIFT_ERR_NULL_POINTER;
+    xa.peers = peers;
+    xa.p = p;
+    xa.rank = rank;
+    xa.epoch = epoch;
+    xa.error = error;
+    return LIFT_OK;
+}
+
+lift_status lift_asum_allreduce(int64_t n, const float* x, float* result, void* ws,
+                                size_t ws_bytes, void* const* peers, int p, int rank,
+                                unsigned long long epoch, int* error, lift_stream_t stream) {
+    if (!result) return LIFT_ERR_NULL_POINTER;
+    XchgArgs xa;
+    const lift_status st = xchg_check(peers, p, rank, epoch, xa, error);
+    if (st != LIFT_OK) return st;
+    return reduce_launch<AsumOp<LIFT_ASUM_ACC>, LIFT_ASUM_B>(
+        n, x, nullptr, result, nullptr, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 0.f,
+        nullptr, xa);
+}
+
+lift_status lift_dot_allreduce(int64_t n, const float* x, const float* y, float* result,
+                               void* ws, size_t ws_bytes, void* const* peers, int p, int rank,
+                               unsigned long long epoch, int* error, lift_stream_t stream) {
+    if (!result) return LIFT_ERR_NULL_POINTER;
+    XchgArgs xa;
+    const lift_status st = xchg_check(peers, p, rank, epoch, xa, error);
+    if (st != LIFT_OK) return st;
+    return reduce_launch<DotOp<LIFT_DOT_ACC>, LIFT_DOT_B>(
+        n, x, y, result, nullptr, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), 0.f,
+        nullptr, xa);
 }
 
 lift_status lift_combine(int p, const double* partials, float* result, lift_stream_t stream) {

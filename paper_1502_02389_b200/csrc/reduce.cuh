@@ -107,7 +107,75 @@ struct ReduceArgs {
     double* out_f64;     // may be null
     float alpha;         // kMapStore ops: the map's scalar
     float* map_out;      // kMapStore ops: where the mapped values are stored (n floats)
+    // NEXT-1 fused cross-GPU combine (null peers: plain single-GPU result)
+    void* const* peers;  // p exchange buffers, peers[rank] = this rank's own
+    int p, rank;
+    unsigned long long epoch;  // > 0, increasing per call on the same buffers
+    int* error;                // set to 1 if the peers did not arrive in time
 };
+
+// ---- NEXT-1: the outermost reduce across GPUs, inside the kernel -------------------
+// Exchange buffer (per rank, lift_xchg_bytes): two banks (epoch parity) of p slots of
+// {double value; u64 flag}.  The final CTA of every rank stores its fp64 partial into
+// slot `rank` of every peer's buffer (NVLink P2P stores to IPC-mapped memory), then
+// raises the slot's flag to `epoch` with a system-scope release; it then waits for all
+// p flags of its own buffer (acquire) and folds the p values pairwise in rank order
+// (zero-padded to 32 — the same tree as lift_combine), so every rank gets the same
+// bits with no separate collective launch.  Two banks suffice: a peer can be at most
+// one call ahead, since finishing call e needs this rank's call-e publish.
+struct XchgSlot {
+    double value;
+    unsigned long long flag;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys_f64(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Warp 0 of the finishing CTA: publish `total`, gather all ranks', fold, write out.
+__device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) {
+    const int lane = threadIdx.x & 31;
+    const int bank = (int)(a.epoch & 1ull) * a.p;
+    if (lane < a.p) {
+        XchgSlot* dst = reinterpret_cast<XchgSlot*>(a.peers[lane]) + bank + a.rank;
+        dst->value = total;
+        __threadfence_system();
+        st_release_sys(&dst->flag, a.epoch);
+    }
+    double v = 0.0;
+    bool ok = true;
+    if (lane < a.p) {
+        XchgSlot* own = reinterpret_cast<XchgSlot*>(a.peers[a.rank]) + bank + lane;
+        // bounded spin (~2 s): a missing peer must not hang the GPU
+        unsigned long long spins = 0;
+        while (ld_acquire_sys(&own->flag) != a.epoch) {
+            __nanosleep(128);
+            if (++spins > (1ull << 24)) {
+                ok = false;
+                break;
+            }
+        }
+        v = ok ? ld_relaxed_sys_f64(&own->value) : 0.0;
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+    const double sum = warp_pairwise(v);  // pairwise over ranks, zero-padded to 32
+    if (lane == 0) {
+        const double r = all_ok ? sum : __longlong_as_double(0x7ff8000000000000ll);  // NaN
+        if (!all_ok && a.error) *a.error = 1;
+        if (a.out_f64) *a.out_f64 = r;
+        if (a.out_f32) *a.out_f32 = __double2float_rn(r);
+    }
+}
 
 // Warp-level pairwise fold of `nleaf` fp64 leaves read from global memory (L2),
 // zero-padded to a power of two p2: lane l folds the aligned block [l*blk, (l+1)*blk)
@@ -134,6 +202,11 @@ __device__ __forceinline__ double warp_fold_leaves(const double* leaves, int64_t
         v = stk[0];
     }
     return warp_pairwise(v);
+}
+
+// n == 0 on one rank of an all-reduce: it still has to publish (a zero) and combine.
+__global__ void xchg_only_kernel(ReduceArgs a) {
+    if (threadIdx.x < 32) xchg_combine(a, 0.0);
 }
 
 template <class Op, int LW, int B0>
@@ -263,10 +336,12 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
         const int64_t g0 = g * RED_G;
         const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
         if (a.ng == 1) {  // one group: the pairwise fold over one leaf is the leaf itself
-            if (lane == 0) {
+            if (lane == 0) a.tick[0] = 0u;
+            if (a.peers) {
+                xchg_combine(a, gpart);
+            } else if (lane == 0) {
                 if (a.out_f64) *a.out_f64 = gpart;
                 if (a.out_f32) *a.out_f32 = __double2float_rn(gpart);
-                a.tick[0] = 0u;
             }
             continue;
         }
@@ -282,10 +357,12 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
         // Last group: final pairwise fold over the group partials, round once.
         __threadfence();
         const double total = warp_fold_leaves(a.group_part, a.ng);
-        if (lane == 0) {
+        if (lane == 0) a.tick[a.ng] = 0u;
+        if (a.peers) {
+            xchg_combine(a, total);
+        } else if (lane == 0) {
             if (a.out_f64) *a.out_f64 = total;
             if (a.out_f32) *a.out_f32 = __double2float_rn(total);
-            a.tick[a.ng] = 0u;
         }
     }
 }

@@ -24,6 +24,8 @@ itself always runs in liblift (``combine_fn`` is injectable only for those tests
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -128,3 +130,87 @@ def sharded_gemv(A_rows: torch.Tensor, x: torch.Tensor, y_rows: torch.Tensor, al
     """Each rank computes its rows' y_out slice, then all ranks gather the full y."""
     ys = _lift().gemv(A_rows, x, y_rows, alpha, beta, out=out_slice)
     return gather_rows(ys, m, group, out=out_full)
+
+
+class PeerExchange:
+    """NEXT-1: the cross-GPU combine fused into the reduction kernel (lift_*_allreduce).
+
+    Each rank creates an exchange buffer (lift_xchg_create), exports it with CUDA IPC,
+    and maps every peer's buffer; the reduction's final CTA then writes its fp64 partial
+    straight into the peers' buffers (NVLink P2P stores on a multi-GPU node), waits for
+    theirs and folds them in rank order — no separate NCCL launch, same bits on every
+    rank as ``sharded_asum``/``sharded_dot``.  The 64-byte IPC handles are exchanged
+    once, through ``torch.distributed`` (any backend).  All ranks must call ``asum`` /
+    ``dot`` in the same sequence.
+    """
+
+    def __init__(self, group=None, device=None):
+        from ._lib import check, lib
+        self._lib, self._check = lib, check
+        self.group = group
+        self.p = _world(group)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = torch.device(device or "cuda", torch.cuda.current_device()
+                                   if device is None else torch.device(device).index)
+        buf = ctypes.c_void_p()
+        check(lib.lift_xchg_create(self.p, ctypes.byref(buf)))
+        self.buf = buf.value
+        handle = (ctypes.c_ubyte * 64)()
+        check(lib.lift_ipc_get_handle(self.buf, handle))
+        handles = [bytes(handle)]
+        if self.p > 1:
+            handles = [None] * self.p
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        self.opened = []
+        ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(self.buf)
+                continue
+            ptr = ctypes.c_void_p()
+            check(lib.lift_ipc_open_handle((ctypes.c_ubyte * 64).from_buffer_copy(h),
+                                           ctypes.byref(ptr)))
+            self.opened.append(ptr.value)
+            ptrs.append(ptr.value)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+        self.error = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.epoch = 0
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def asum(self, x_shard, out=None, ws=None):
+        lift = _lift()
+        x = lift._vec(x_shard, "x")
+        r = lift._out(out, 1, torch.float32, x.device)
+        w = ws or lift._workspace(x.numel(), x.device)
+        self.epoch += 1
+        self._check(self._lib.lift_asum_allreduce(
+            x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes, self.peers.data_ptr(),
+            self.p, self.rank, self.epoch, self.error.data_ptr(), self._stream()))
+        return r
+
+    def dot(self, x_shard, y_shard, out=None, ws=None):
+        lift = _lift()
+        x, y = lift._vec(x_shard, "x"), lift._vec(y_shard, "y")
+        if x.numel() != y.numel():
+            raise ValueError("zip-length-mismatch: dot needs equal lengths (PAPER.md P:307)")
+        r = lift._out(out, 1, torch.float32, x.device)
+        w = ws or lift._workspace(x.numel(), x.device)
+        self.epoch += 1
+        self._check(self._lib.lift_dot_allreduce(
+            x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+            self.peers.data_ptr(), self.p, self.rank, self.epoch, self.error.data_ptr(),
+            self._stream()))
+        return r
+
+    def close(self):
+        torch.cuda.synchronize(self.device)
+        if self.p > 1 and dist.is_initialized():
+            dist.barrier(group=self.group)  # nobody still writes into our buffer
+        for ptr in self.opened:
+            self._lib.lift_ipc_close_handle(ptr)
+        self.opened = []
+        if self.buf:
+            self._lib.lift_xchg_destroy(self.buf)
+            self.buf = None

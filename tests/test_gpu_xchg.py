@@ -1,0 +1,106 @@
+"""NEXT-1 row: the cross-GPU combine fused into the reduction kernel (peer-memory
+exchange over CUDA IPC), run as two processes on the one available B200.
+
+Bars: every rank gets the same bits; they equal the NCCL-style path (lift_*_partial,
+all-gather, lift_combine) and, for power-of-two group shards, the unsharded call;
+repeated calls (epochs, alternating banks) stay correct; a rank with an empty shard
+still participates.  On a multi-GPU node the same stores travel over NVLink."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import lift_inputs as gen
+    import paper_1502_02389_b200 as lift
+    from paper_1502_02389_b200 import dist as ldist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dev = torch.device("cuda:0")
+        torch.cuda.set_device(dev)
+        ex = ldist.PeerExchange(device=dev)
+        out = []
+        for it, groups in enumerate([8, 8, 2, 1, 8]):  # several epochs / both banks
+            n = groups * lift.GROUP_ELEMS + (0 if it != 4 else 12345)
+            a, b = ldist.shard_range(n, rank, world)
+            x = gen.fill_device(torch.empty(b - a, device=dev), it, gen.TID_X, a)
+            y = gen.fill_device(torch.empty(b - a, device=dev), it, gen.TID_Y, a)
+            ra = ex.asum(x)
+            rd = ex.dot(x, y)
+            ga = ldist.sharded_asum(x)   # NCCL-style reference path (gloo transport here)
+            gd = ldist.sharded_dot(x, y)
+            out.append([t.cpu().numpy().view(np.uint32).tolist() for t in (ra, rd, ga, gd)])
+        # rank 1 with an empty shard
+        e = torch.empty(0, device=dev)
+        x = gen.fill_device(torch.empty(1000, device=dev), 9, gen.TID_X, 0)
+        re = ex.asum(x if rank == 0 else e)
+        out.append(re.cpu().numpy().view(np.uint32).tolist())
+        out.append(int(ex.error.item()))
+        ex.close()
+        q.put((rank, out))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surface errors to the parent
+        import traceback
+        q.put((rank, "error: " + repr(e) + traceback.format_exc()))
+
+
+def test_fused_exchange_two_processes_one_gpu():
+    import lift_inputs as gen
+    import paper_1502_02389_b200 as lift
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=300)
+        res[r[0]] = r[1]
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+    assert res[0] == res[1]                      # same bits on every rank
+    for it, (ra, rd, ga, gd) in enumerate(res[0][:5]):
+        assert ra == ga and rd == gd, it         # == all-gather + lift_combine path
+    dev = torch.device("cuda:0")
+    for it, groups in enumerate([8, 8, 2]):      # power-of-two group shards: == unsharded
+        n = groups * lift.GROUP_ELEMS
+        x = gen.fill_device(torch.empty(n, device=dev), it, gen.TID_X, 0)
+        y = gen.fill_device(torch.empty(n, device=dev), it, gen.TID_Y, 0)
+        assert res[0][it][0] == lift.asum(x).cpu().numpy().view(np.uint32).tolist()
+        assert res[0][it][1] == lift.dot(x, y).cpu().numpy().view(np.uint32).tolist()
+    x = gen.fill_device(torch.empty(1000, device=dev), 9, gen.TID_X, 0)
+    assert res[0][5] == lift.asum(x).cpu().numpy().view(np.uint32).tolist()  # empty peer
+    assert res[0][6] == 0 and res[1][6] == 0     # no timeouts
+
+
+def test_fused_exchange_single_rank():
+    import lift_inputs as gen
+    import paper_1502_02389_b200 as lift
+    from paper_1502_02389_b200 import dist as ldist
+    dev = torch.device("cuda:0")
+    ex = ldist.PeerExchange(device=dev)
+    x = gen.fill_device(torch.empty(3 * lift.GROUP_ELEMS + 7, device=dev), 1, gen.TID_X, 0)
+    for _ in range(3):
+        assert ex.asum(x).item() == lift.asum(x).item()
+    ex.close()
