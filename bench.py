@@ -244,6 +244,17 @@ def run_lift(args):
     r_dot = torch.empty(1, dtype=torch.float32, device=dev)
     ws_a = lift.Workspace(N_VEC, dev)
     ws_d = lift.Workspace(N_DOT, dev)
+    # X1 for asum/dot at N > 1: the combine fused into the reduction kernel (NEXT-1,
+    # peer-memory exchange); LIFT_X1=nccl selects all-gather + lift_combine instead.
+    x1_mode = os.environ.get("LIFT_X1", "fused") if world > 1 else "none"
+    xchg = ldist.PeerExchange(group, device=dev) if x1_mode == "fused" else None
+
+    def x_asum(x, out, ws):
+        return xchg.asum(x, out=out, ws=ws) if xchg else ldist.sharded_asum(x, group, out=out, ws=ws)
+
+    def x_dot(x, y, out, ws):
+        return (xchg.dot(x, y, out=out, ws=ws) if xchg
+                else ldist.sharded_dot(x, y, group, out=out, ws=ws))
     torch.cuda.synchronize()
 
     def step(ev=None):
@@ -257,12 +268,12 @@ def run_lift(args):
         if world == 1:
             lift.asum(x_v, out=r_asum, ws=ws_a)
         else:
-            ldist.sharded_asum(x_v, group, out=r_asum, ws=ws_a)
+            x_asum(x_v, r_asum, ws_a)
         rec(2)
         if world == 1:
             lift.dot(x_d, y_d, out=r_dot, ws=ws_d)
         else:
-            ldist.sharded_dot(x_d, y_d, group, out=r_dot, ws=ws_d)
+            x_dot(x_d, y_d, r_dot, ws_d)
         rec(3)
         if world == 1:
             lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out)
@@ -336,7 +347,7 @@ def run_lift(args):
     _dbg("per-op times reduced")
     if not args.no_e2e:
         e2e = run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
-                      max_over_ranks, barrier, step_bytes)
+                      max_over_ranks, barrier, step_bytes, x_asum, x_dot)
 
     peak, peak_src = load_peaks()
     traffic = load_traffic()
@@ -350,7 +361,7 @@ def run_lift(args):
               for op in OPS}
 
     if rank == 0:
-        launches_per_step = 4 + (2 if world > 1 else 0)
+        launches_per_step = 4 + (2 if x1_mode == "nccl" else 0)
         line = {
             "metric": "achieved HBM GB/s (fraction of 8 TB/s) for asum/dot/scal/gemv at "
                       "1/2/4/8 B200",
@@ -363,6 +374,9 @@ def run_lift(args):
                                    "n=2^26 (configs[1]) + gemv 8192x8192 a=1.5 b=0.5 "
                                    "(configs[3]), per rank",
                        "global_batch": world, "parallelism": f"shard{world} (weak)",
+                       "x1": {"none": "single GPU", "fused": "asum/dot combine fused into the "
+                              "reduction kernel over peer memory; gemv y all-gather (NCCL)",
+                              "nccl": "all-gather + lift_combine; gemv y all-gather"}[x1_mode],
                        "l2": "no flush: every operand >= 256 MiB > 126 MB L2",
                        "frac_of_8TBs": round(value / world / NOMINAL_HBM, 4)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1),
@@ -377,6 +391,8 @@ def run_lift(args):
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_budget)
         print(json.dumps(line), flush=True)
+    if xchg is not None:
+        xchg.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -384,7 +400,7 @@ def run_lift(args):
 
 
 def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
-            max_over_ranks, barrier, step_bytes):
+            max_over_ranks, barrier, step_bytes, x_asum, x_dot):
     """Same metric, end to end: every step copies its inputs from pinned host memory,
     runs the step through the public API and reads every result back to the host."""
     steps = max(1, min(args.steps, args.e2e_steps))
@@ -455,9 +471,9 @@ def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream
                 s_cmp.wait_event(ev_g)
                 lift.gemv(A, d["gx"], d["gy"], ALPHA, BETA, out=d_gf)
             else:
-                ldist.sharded_asum(d["x"], group, out=d_res[0:1], ws=ws_a)
+                x_asum(d["x"], d_res[0:1], ws_a)
                 s_cmp.wait_event(ev_dot)
-                ldist.sharded_dot(d["dx"], d["dy"], group, out=d_res[1:2], ws=ws_d)
+                x_dot(d["dx"], d["dy"], d_res[1:2], ws_d)
                 s_cmp.wait_event(ev_g)
                 ldist.sharded_gemv(A, d["gx"], d["gy"], ALPHA, BETA, GEMV_M * world, group,
                                    out_full=d_gf, out_slice=d_g)

@@ -150,8 +150,9 @@ class PeerExchange:
         self.group = group
         self.p = _world(group)
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.device = torch.device(device or "cuda", torch.cuda.current_device()
-                                   if device is None else torch.device(device).index)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
         buf = ctypes.c_void_p()
         check(lib.lift_xchg_create(self.p, ctypes.byref(buf)))
         self.buf = buf.value
