@@ -22,11 +22,15 @@ def fill(n, tid, lo, hi):
     return gen.fill_device(torch.empty(n, dtype=torch.float32, device=dev), 0, tid, 0, 0, lo, hi)
 
 
-flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # 256 MiB > 2x L2
+# L2 flush by READING 512 MiB (> 4x L2): leaves only clean lines behind, so the timed
+# launch does not pay for write-backs of a flush buffer (zero-filling one would).
+flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)
 
 
 def time_op(fn, nbytes, reps=20, flush_l2=True):
-    """Median over `reps` of one graph-replayed launch; L2 flushed before each."""
+    """Median over `reps` of one graph-replayed launch; L2 flushed (by reads) before each.
+    A single launch includes its ramp-up and drain, so these are lower than the
+    back-to-back figures of scripts/ab.py and bench.py."""
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
         fn()  # warm (workspace, occupancy cache)
@@ -37,7 +41,7 @@ def time_op(fn, nbytes, reps=20, flush_l2=True):
     ts = []
     for _ in range(reps):
         if flush_l2:
-            flush.zero_()
+            flush.sum()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
         g.replay()
