@@ -488,6 +488,7 @@ def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream
             ev_out.record(s_d2h)
         prev_done[0] = ev_out
 
+    barrier()  # ranks enter the first exchange together (host buffer filling can skew them)
     e2e_step()
     torch.cuda.synchronize()
     barrier()

@@ -16,14 +16,17 @@
  *    P:1077-1080).  All array pointers are DEVICE pointers of the current CUDA
  *    device, at least 4-byte aligned; wider alignment only enables wider loads and
  *    never changes a result bit.
- *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default
- *    stream): it validates its arguments on the host, enqueues exactly one kernel
- *    (none for empty work) and returns.  It never synchronises, never allocates and
- *    never touches host copies of the data.  Results are stream-ordered in device
+ *  - Every compute call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream): it validates its arguments on the host, enqueues exactly one
+ *    kernel (none for empty work; a cudaMemsetAsync for an empty reduction) and
+ *    returns.  It never synchronises, never allocates and never touches host copies of
+ *    the data.  The exceptions are the one-time setup calls of the NEXT-1 exchange
+ *    (lift_xchg_create/destroy, lift_ipc_*), which allocate, map or free synchronously.  Results are stream-ordered in device
  *    memory; read them after your own sync.  A reduction's result is a 1-element
  *    device array, following the paper's "primitives are arrays of length 1"
  *     and reduce's type T[] -> T[1].
- *  - The caller owns every buffer, including the workspace.  The library keeps no
+ *  - The caller owns every buffer, including the workspace and the exchange buffers
+ *    (which lift_xchg_create allocates on the caller's behalf).  The library keeps no
  *    device memory and no mutable state except a per-device cache of the SM count
  *    and kernel occupancies (and the test hook lift_debug_set_grid_limit).
  *  - Errors are returned synchronously and nothing is launched:
@@ -130,7 +133,7 @@ lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, flo
  *   lift_combine over the gathered *_partial results — with no separate collective.
  *   p in [1, 32]; epoch > 0 and strictly increasing per call on the same buffers (two
  *   banks alternate by epoch parity); all p ranks must make the matching call.  The
- *   wait is bounded (~2 s): on timeout *result = NaN and *error (device int, may be
+ *   wait is bounded (~10 s): on timeout *result = NaN and *error (device int, may be
  *   NULL) is set to 1.  Workspace as for lift_asum. */
 #define LIFT_IPC_HANDLE_BYTES 64
 size_t lift_xchg_bytes(int p);

@@ -156,11 +156,11 @@ __device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) 
     bool ok = true;
     if (lane < a.p) {
         XchgSlot* own = reinterpret_cast<XchgSlot*>(a.peers[a.rank]) + bank + lane;
-        // bounded spin (~2 s): a missing peer must not hang the GPU
+        // bounded spin (~10 s): a missing peer must not hang the GPU
         unsigned long long spins = 0;
         while (ld_acquire_sys(&own->flag) != a.epoch) {
             __nanosleep(128);
-            if (++spins > (1ull << 24)) {
+            if (++spins > (1ull << 26)) {
                 ok = false;
                 break;
             }
