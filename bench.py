@@ -255,6 +255,12 @@ def run_lift(args):
     def x_dot(x, y, out, ws):
         return (xchg.dot(x, y, out=out, ws=ws) if xchg
                 else ldist.sharded_dot(x, y, group, out=out, ws=ws))
+
+    def x_gemv(A, gx, gy, out_full, out_slice):
+        if xchg:  # rows land in every rank's full y inside the gemv kernel
+            return xchg.gemv(A, gx, gy, ALPHA, BETA, GEMV_M * world, rank * GEMV_M)
+        return ldist.sharded_gemv(A, gx, gy, ALPHA, BETA, GEMV_M * world, group,
+                                  out_full=out_full, out_slice=out_slice)
     torch.cuda.synchronize()
 
     def step(ev=None):
@@ -278,8 +284,7 @@ def run_lift(args):
         if world == 1:
             lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out)
         else:
-            ldist.sharded_gemv(A, g_x, g_y, ALPHA, BETA, GEMV_M * world, group,
-                               out_full=g_full, out_slice=g_out)
+            x_gemv(A, g_x, g_y, g_full, g_out)
         rec(4)
 
     def barrier():
@@ -347,7 +352,7 @@ def run_lift(args):
     _dbg("per-op times reduced")
     if not args.no_e2e:
         e2e = run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
-                      max_over_ranks, barrier, step_bytes, x_asum, x_dot)
+                      max_over_ranks, barrier, step_bytes, x_asum, x_dot, x_gemv)
 
     peak, peak_src = load_peaks()
     traffic = load_traffic()
@@ -400,7 +405,7 @@ def run_lift(args):
 
 
 def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
-            max_over_ranks, barrier, step_bytes, x_asum, x_dot):
+            max_over_ranks, barrier, step_bytes, x_asum, x_dot, x_gemv):
     """Same metric, end to end: every step copies its inputs from pinned host memory,
     runs the step through the public API and reads every result back to the host."""
     steps = max(1, min(args.steps, args.e2e_steps))
@@ -475,8 +480,9 @@ def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream
                 s_cmp.wait_event(ev_dot)
                 x_dot(d["dx"], d["dy"], d_res[1:2], ws_d)
                 s_cmp.wait_event(ev_g)
-                ldist.sharded_gemv(A, d["gx"], d["gy"], ALPHA, BETA, GEMV_M * world, group,
-                                   out_full=d_gf, out_slice=d_g)
+                yf = x_gemv(A, d["gx"], d["gy"], d_gf, d_g)
+                if yf.data_ptr() != d_gf.data_ptr():
+                    d_gf.copy_(yf)
             ev_res.record(s_cmp)
         with torch.cuda.stream(s_d2h):
             for i in range(NCH):

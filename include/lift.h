@@ -138,6 +138,9 @@ lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, flo
 #define LIFT_IPC_HANDLE_BYTES 64
 size_t lift_xchg_bytes(int p);
 lift_status lift_xchg_create(int p, void** buf);
+/* cudaMalloc'd buffer for IPC sharing (a base pointer, as cudaIpcGetMemHandle needs);
+ * free with lift_xchg_destroy. */
+lift_status lift_ipc_alloc(size_t bytes, void** buf);
 lift_status lift_xchg_destroy(void* buf);
 lift_status lift_ipc_get_handle(const void* buf, void* handle);
 lift_status lift_ipc_open_handle(const void* handle, void** ptr);
@@ -148,6 +151,20 @@ lift_status lift_asum_allreduce(int64_t n, const float* x, float* result, void* 
 lift_status lift_dot_allreduce(int64_t n, const float* x, const float* y, float* result,
                                void* ws, size_t ws_bytes, void* const* peers, int p, int rank,
                                unsigned long long epoch, int* error, lift_stream_t stream);
+
+/* NEXT-1 — gemv with the all-gather of y fused in: rank `rank` owns rows
+ *   [row0, row0 + m) of the global A; each finished row is stored straight into every
+ *   rank's full-length y (y_peers: DEVICE array of p pointers, IPC-mapped, from
+ *   lift_ipc_alloc), and the CTA that finishes the rank's last row block publishes the
+ *   rank's flag into every exchange buffer (xpeers, as for lift_*_allreduce, including
+ *   the same epoch rule) and waits for all p flags.  When the kernel ends, this rank's
+ *   y holds every rank's rows — bit-identical to lift_gemv + an all-gather.  m >= 1 on
+ *   every rank; y_out is implied (y_peers[rank] + row0). */
+lift_status lift_gemv_allgather(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
+                                const float* x, float beta, const float* y,
+                                float* const* y_peers, int64_t row0, void* const* xpeers,
+                                int p, int rank, unsigned long long epoch, int* error,
+                                lift_stream_t stream);
 
 /* X1 — combine: *result = RN_fp32(pairwise_sum(partials[0..p))), the outermost
  *   reduce over per-rank partials in a fixed pairwise order (zero-padded to a power

@@ -18,7 +18,8 @@ EXPORTS = (
     "lift_gemv", "lift_debug_set_grid_limit", "lift_reduce_chunk_elems",
     "lift_reduce_group_chunks", "lift_blackscholes", "lift_scal_asum", "lift_xchg_bytes",
     "lift_xchg_create", "lift_xchg_destroy", "lift_ipc_get_handle", "lift_ipc_open_handle",
-    "lift_ipc_close_handle", "lift_asum_allreduce", "lift_dot_allreduce",
+    "lift_ipc_close_handle", "lift_asum_allreduce", "lift_dot_allreduce", "lift_ipc_alloc",
+    "lift_gemv_allgather",
 )
 
 LIFT_OK = 0
@@ -59,6 +60,9 @@ def _load():
                                  _vp, _vp], _int),
         "lift_dot_allreduce": ([_i64, _vp, _vp, _vp, _vp, _sz, _vp, _int, _int,
                                 ctypes.c_ulonglong, _vp, _vp], _int),
+        "lift_ipc_alloc": ([_sz, ctypes.POINTER(ctypes.c_void_p)], _int),
+        "lift_gemv_allgather": ([_i64, _i64, _f32, _vp, _i64, _vp, _f32, _vp, _vp, _i64, _vp,
+                                 _int, _int, ctypes.c_ulonglong, _vp, _vp], _int),
         "lift_blackscholes": ([_i64, _vp, _f32, _f32, _f32, _f32, _vp, _vp, _vp], _int),
     }
     for name, (args, res) in sig.items():

@@ -134,6 +134,44 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// ---- NEXT-1 peer-memory exchange primitives (reduce.cuh, gemv.cuh) -----------------
+// Exchange buffer of one rank: [2 banks x p slots of XchgSlot][2 u64 counters].
+struct XchgSlot {
+    double value;
+    unsigned long long flag;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys_f64(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long* xchg_counter(void* buf, int p, int bank) {
+    return reinterpret_cast<unsigned long long*>(reinterpret_cast<XchgSlot*>(buf) + 2 * p) + bank;
+}
+
+// Lane q < p: wait until slot q of this rank's bank carries `epoch` (bounded ~10 s).
+// Returns false on timeout.
+__device__ __forceinline__ bool xchg_wait_flag(void* own_buf, int bank_base, int q,
+                                               unsigned long long epoch) {
+    XchgSlot* own = reinterpret_cast<XchgSlot*>(own_buf) + bank_base + q;
+    unsigned long long spins = 0;
+    while (ld_acquire_sys(&own->flag) != epoch) {
+        __nanosleep(128);
+        if (++spins > (1ull << 26)) return false;
+    }
+    return true;
+}
+
 // ---- Cluster Launch Control (sm_100): hardware work stealing -------------------------
 // A resident CTA cancels a not-yet-launched CTA of the same grid and takes over its
 // blockIdx (SASS UGETNEXTWORKID).  This gives persistent CTAs (per-CTA setup such as

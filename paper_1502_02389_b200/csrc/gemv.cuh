@@ -62,6 +62,14 @@ struct GemvArgs {
     float* y_out;
     int P;          // panel columns (multiple of 256, <= GEMV_PMAX)
     int xs_stride;  // doubles per slot row of xs (= P/8 + 1, padding breaks bank conflicts)
+    // NEXT-1 fused all-gather of y (null y_peers: plain local y_out)
+    float* const* y_peers;  // p pointers: every rank's full-length y (IPC-mapped)
+    int64_t row0;           // global row of local row 0
+    void* const* xpeers;    // p exchange buffers (flags + block counters)
+    int p, rank;
+    unsigned long long epoch;
+    int* error;
+    int64_t nblocks;        // row blocks of this launch
 };
 
 __host__ __device__ constexpr size_t gemv_smem_bytes(int P) {
@@ -171,9 +179,42 @@ __device__ __forceinline__ void gemv_epilogue(const GemvArgs& a, const int64_t* 
         const double d = warp_pairwise(pairwise8(acc[r]));
         if (lane == r && r < nvalid) {
             const double w = __dmul_rn((double)a.beta, (double)a.y[rows[r]]);  // scal(b, y): exact
-            a.y_out[rows[r]] = __double2float_rn(__fma_rn((double)a.alpha, d, w));
+            const float out = __double2float_rn(__fma_rn((double)a.alpha, d, w));
+            if (a.y_peers) {  // fused all-gather: the row lands in every rank's full y
+                for (int q = 0; q < a.p; ++q) a.y_peers[q][a.row0 + rows[r]] = out;
+            } else {
+                a.y_out[rows[r]] = out;
+            }
         }
     }
+}
+
+// NEXT-1 fused all-gather: after each row block the CTA counts it in this rank's
+// exchange buffer; the CTA that completes the LAST block publishes the rank's flag into
+// every peer's buffer (system-scope release; the row stores were fenced at system scope
+// before each count) and waits for all p flags, so the kernel ends only when every
+// rank's rows have landed in this rank's y — stream-ordered consumers can read it.
+__device__ __forceinline__ void gemv_block_done(const GemvArgs& a) {
+    const int lane = threadIdx.x & 31;
+    const int bank = (int)(a.epoch & 1ull);
+    unsigned last = 0;
+    if (lane == 0) {
+        __threadfence_system();  // this block's row stores before its count
+        unsigned long long* cnt = xchg_counter(a.xpeers[a.rank], a.p, bank);
+        last = (atomicAdd(cnt, 1ull) == (unsigned long long)(a.nblocks - 1));
+        if (last) {
+            __threadfence_system();
+            *cnt = 0ull;  // reset for epoch + 2 (this bank's next use)
+        }
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    bool ok = true;
+    if (lane < a.p) {
+        XchgSlot* dst = reinterpret_cast<XchgSlot*>(a.xpeers[lane]) + bank * a.p + a.rank;
+        st_release_sys(&dst->flag, a.epoch);
+        ok = xchg_wait_flag(a.xpeers[a.rank], bank * a.p, lane, a.epoch);
+    }
+    if (!__all_sync(0xffffffffu, ok) && lane == 0 && a.error) *a.error = 1;
 }
 
 // MULTI = false: n <= P, x staged once per CTA.  MULTI = true: n > P, x re-staged per
@@ -225,6 +266,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) gemv_kernel(GemvArgs 
         int64_t next;
         const bool more = clc_fetch(clc, next);
         __syncthreads();  // everyone has read the response before it is reused
+        if (a.y_peers && warp == 0) gemv_block_done(a);  // after the barrier: rows stored
         if (!more) break;
         blk = next;
     }

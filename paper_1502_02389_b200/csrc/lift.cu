@@ -247,7 +247,9 @@ lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
     const int64_t rows_per_cta = (int64_t)(NT / 32) * GEMV_R;
     const int64_t blocks = (a.m + rows_per_cta - 1) / rows_per_cta;
     const int64_t grid = grid_for(blocks, fn, NT, smem, false, true);  // CLC steals the rest
-    gemv_kernel<NT, GEMV_R, GEMV_U, LW, MULTI><<<(unsigned)grid, NT, smem, s>>>(a);
+    GemvArgs b = a;
+    b.nblocks = blocks;
+    gemv_kernel<NT, GEMV_R, GEMV_U, LW, MULTI><<<(unsigned)grid, NT, smem, s>>>(b);
     return launched();
 }
 
@@ -367,7 +369,9 @@ lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, flo
         y);
 }
 
-size_t lift_xchg_bytes(int p) { return p < 1 ? 0 : (size_t)2 * p * sizeof(XchgSlot); }
+size_t lift_xchg_bytes(int p) {
+    return p < 1 ? 0 : (size_t)2 * p * sizeof(XchgSlot) + 2 * sizeof(unsigned long long);
+}
 
 lift_status lift_xchg_create(int p, void** buf) {
     if (p < 1 || p > 32) return LIFT_ERR_INVALID_VALUE;
@@ -378,6 +382,15 @@ lift_status lift_xchg_create(int p, void** buf) {
         cudaFree(d);
         return LIFT_ERR_CUDA;
     }
+    *buf = d;
+    return LIFT_OK;
+}
+
+lift_status lift_ipc_alloc(size_t bytes, void** buf) {
+    if (!buf) return LIFT_ERR_NULL_POINTER;
+    if (bytes == 0) return LIFT_ERR_INVALID_VALUE;
+    void* d = nullptr;
+    if (cudaMalloc(&d, bytes) != cudaSuccess) return LIFT_ERR_CUDA;
     *buf = d;
     return LIFT_OK;
 }
@@ -455,6 +468,37 @@ lift_status lift_combine(int p, const double* partials, float* result, lift_stre
     return launched();
 }
 
+lift_status lift_gemv_allgather(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
+                                const float* x, float beta, const float* y, float* const* y_peers,
+                                int64_t row0, void* const* xpeers, int p, int rank,
+                                unsigned long long epoch, int* error, lift_stream_t stream) {
+    if (m < 0 || n < 0 || row0 < 0) return LIFT_ERR_INVALID_VALUE;
+    if (lda < (n > 1 ? n : 1)) return LIFT_ERR_INVALID_VALUE;
+    if (p < 1 || p > 32 || rank < 0 || rank >= p || epoch == 0) return LIFT_ERR_INVALID_VALUE;
+    if (!y_peers || !xpeers) return LIFT_ERR_NULL_POINTER;
+    if (m == 0) return LIFT_ERR_INVALID_VALUE;  // every rank must contribute >= 1 row
+    if (!y || (n > 0 && (!A || !x))) return LIFT_ERR_NULL_POINTER;
+    if (misaligned4(A) || misaligned4(x) || misaligned4(y)) return LIFT_ERR_INVALID_VALUE;
+    GemvArgs a{};
+    a.m = m;
+    a.n = n;
+    a.lda = lda;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.A = A;
+    a.x = x;
+    a.y = y;
+    a.y_out = nullptr;
+    a.y_peers = y_peers;
+    a.row0 = row0;
+    a.xpeers = xpeers;
+    a.p = p;
+    a.rank = rank;
+    a.epoch = epoch;
+    a.error = error;
+    return gemv_launch(a, reinterpret_cast<cudaStream_t>(stream));
+}
+
 lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
                       const float* x, float beta, const float* y, float* y_out,
                       lift_stream_t stream) {
@@ -464,7 +508,7 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
     if (!y || !y_out || (n > 0 && (!A || !x))) return LIFT_ERR_NULL_POINTER;
     if (misaligned4(A) || misaligned4(x) || misaligned4(y) || misaligned4(y_out))
         return LIFT_ERR_INVALID_VALUE;
-    GemvArgs a;
+    GemvArgs a{};
     a.m = m;
     a.n = n;
     a.lda = lda;

@@ -123,25 +123,6 @@ struct ReduceArgs {
 // (zero-padded to 32 — the same tree as lift_combine), so every rank gets the same
 // bits with no separate collective launch.  Two banks suffice: a peer can be at most
 // one call ahead, since finishing call e needs this rank's call-e publish.
-struct XchgSlot {
-    double value;
-    unsigned long long flag;
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ double ld_relaxed_sys_f64(const double* p) {
-    double v;
-    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // Warp 0 of the finishing CTA: publish `total`, gather all ranks', fold, write out.
 __device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) {
     const int lane = threadIdx.x & 31;
@@ -154,17 +135,9 @@ __device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) 
     }
     double v = 0.0;
     bool ok = true;
-    if (lane < a.p) {
+    if (lane < a.p) {  // bounded spin (~10 s): a missing peer must not hang the GPU
+        ok = xchg_wait_flag(a.peers[a.rank], bank, lane, a.epoch);
         XchgSlot* own = reinterpret_cast<XchgSlot*>(a.peers[a.rank]) + bank + lane;
-        // bounded spin (~10 s): a missing peer must not hang the GPU
-        unsigned long long spins = 0;
-        while (ld_acquire_sys(&own->flag) != a.epoch) {
-            __nanosleep(128);
-            if (++spins > (1ull << 26)) {
-                ok = false;
-                break;
-            }
-        }
         v = ok ? ld_relaxed_sys_f64(&own->value) : 0.0;
     }
     const bool all_ok = __all_sync(0xffffffffu, ok);

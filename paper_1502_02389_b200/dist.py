@@ -156,26 +156,11 @@ class PeerExchange:
         buf = ctypes.c_void_p()
         check(lib.lift_xchg_create(self.p, ctypes.byref(buf)))
         self.buf = buf.value
-        handle = (ctypes.c_ubyte * 64)()
-        check(lib.lift_ipc_get_handle(self.buf, handle))
-        handles = [bytes(handle)]
-        if self.p > 1:
-            handles = [None] * self.p
-            dist.all_gather_object(handles, bytes(handle), group=group)
-        self.opened = []
-        ptrs = []
-        for r, h in enumerate(handles):
-            if r == self.rank:
-                ptrs.append(self.buf)
-                continue
-            ptr = ctypes.c_void_p()
-            check(lib.lift_ipc_open_handle((ctypes.c_ubyte * 64).from_buffer_copy(h),
-                                           ctypes.byref(ptr)))
-            self.opened.append(ptr.value)
-            ptrs.append(ptr.value)
+        ptrs, self.opened = self._share(self.buf)
         self.peers = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
         self.error = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.epoch = 0
+        self._y = None  # (m, own ptr, opened peer ptrs, device array, tensor view)
 
     def _stream(self):
         return torch.cuda.current_stream(self.device).cuda_stream
@@ -205,7 +190,74 @@ class PeerExchange:
             self._stream()))
         return r
 
+    def _share(self, own_ptr):
+        """Exchange IPC handles of `own_ptr` (a lift-allocated base pointer); returns
+        the p pointers (own at `rank`) and the list of opened peer mappings."""
+        handle = (ctypes.c_ubyte * 64)()
+        self._check(self._lib.lift_ipc_get_handle(own_ptr, handle))
+        handles = [bytes(handle)]
+        if self.p > 1:
+            handles = [None] * self.p
+            dist.all_gather_object(handles, bytes(handle), group=self.group)
+        ptrs, opened = [], []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(own_ptr)
+                continue
+            ptr = ctypes.c_void_p()
+            self._check(self._lib.lift_ipc_open_handle(
+                (ctypes.c_ubyte * 64).from_buffer_copy(h), ctypes.byref(ptr)))
+            opened.append(ptr.value)
+            ptrs.append(ptr.value)
+        return ptrs, opened
+
+    def _full_y(self, m: int):
+        if self._y is not None and self._y[0] == m:
+            return self._y
+        self._free_y()
+        buf = ctypes.c_void_p()
+        self._check(self._lib.lift_ipc_alloc(max(4, 4 * m), ctypes.byref(buf)))
+        ptrs, opened = self._share(buf.value)
+        arr = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+        view = torch.as_tensor(_DevArray(buf.value, m, self.device.index), device=self.device)
+        self._y = (m, buf.value, opened, arr, view)
+        return self._y
+
+    def _free_y(self):
+        if self._y is None:
+            return
+        torch.cuda.synchronize(self.device)
+        if self.p > 1 and dist.is_initialized():
+            dist.barrier(group=self.group)
+        for ptr in self._y[2]:
+            self._lib.lift_ipc_close_handle(ptr)
+        self._lib.lift_xchg_destroy(self._y[1])
+        self._y = None
+
+    def gemv(self, A_rows, x, y_rows, alpha: float, beta: float, m: int, row0: int):
+        """y_full = alpha*A@x + beta*y over all ranks' rows, the all-gather fused into the
+        gemv kernel (lift_gemv_allgather).  Returns this rank's full-length y (a view of
+        the IPC-shared buffer; valid until the next call with another m or close())."""
+        lift = _lift()
+        if not (A_rows.is_cuda and A_rows.dtype == torch.float32 and A_rows.dim() == 2):
+            raise ValueError("A must be a 2-D float32 CUDA tensor")
+        ml, n = A_rows.shape
+        if ml > 0 and n > 0 and A_rows.stride(1) != 1:
+            raise ValueError("A must be row-major with unit column stride")
+        lda = A_rows.stride(0) if (ml > 1 and n > 0) else max(1, n)
+        x, y = lift._vec(x, "x"), lift._vec(y_rows, "y")
+        if x.numel() != n or y.numel() != ml:
+            raise ValueError("dimension-mismatch")
+        _, _, _, arr, view = self._full_y(m)
+        self.epoch += 1
+        self._check(self._lib.lift_gemv_allgather(
+            ml, n, float(alpha), A_rows.data_ptr(), lda, x.data_ptr(), float(beta), y.data_ptr(),
+            arr.data_ptr(), row0, self.peers.data_ptr(), self.p, self.rank, self.epoch,
+            self.error.data_ptr(), self._stream()))
+        return view
+
     def close(self):
+        self._free_y()
         torch.cuda.synchronize(self.device)
         if self.p > 1 and dist.is_initialized():
             dist.barrier(group=self.group)  # nobody still writes into our buffer
@@ -215,3 +267,12 @@ class PeerExchange:
         if self.buf:
             self._lib.lift_xchg_destroy(self.buf)
             self.buf = None
+
+
+class _DevArray:
+    """Minimal __cuda_array_interface__ wrapper so torch can view a lift-allocated buffer."""
+
+    def __init__(self, ptr: int, n: int, device_index: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+        self.device_index = device_index

@@ -113,13 +113,17 @@ def test_argument_errors_are_synchronous():
     assert lib.lift_scal_asum(10, 2.0, p, p, p, p, 1 << 20, None) == INVALID     # y == x
     assert lib.lift_scal_asum(10, 2.0, p, None, p, p, 1 << 20, None) == NULLP
     assert lib.lift_scal_asum(10, 2.0, p, p + 64, None, p, 1 << 20, None) == NULLP
-    assert lib.lift_xchg_bytes(4) == 2 * 4 * 16 and lib.lift_xchg_bytes(0) == 0
+    assert lib.lift_xchg_bytes(4) == 2 * 4 * 16 + 16 and lib.lift_xchg_bytes(0) == 0
     assert lib.lift_xchg_create(0, None) == INVALID and lib.lift_xchg_create(33, None) == INVALID
     assert lib.lift_ipc_get_handle(None, None) == NULLP
     assert lib.lift_asum_allreduce(10, p, p, p, 1 << 20, p, 2, 2, 1, None, None) == INVALID
     assert lib.lift_asum_allreduce(10, p, p, p, 1 << 20, p, 2, 0, 0, None, None) == INVALID
     assert lib.lift_asum_allreduce(10, p, p, p, 1 << 20, None, 2, 0, 1, None, None) == NULLP
     assert lib.lift_dot_allreduce(10, p, p, None, p, 1 << 20, p, 2, 0, 1, None, None) == NULLP
+    assert lib.lift_gemv_allgather(4, 4, 1.0, p, 4, p, 1.0, p, p, 0, p, 2, 2, 1, None, None) == INVALID
+    assert lib.lift_gemv_allgather(0, 4, 1.0, p, 4, p, 1.0, p, p, 0, p, 2, 0, 1, None, None) == INVALID
+    assert lib.lift_gemv_allgather(4, 4, 1.0, p, 4, p, 1.0, p, None, 0, p, 2, 0, 1, None, None) == NULLP
+    assert lib.lift_ipc_alloc(0, None) == NULLP
     assert lib.lift_debug_set_grid_limit(-1) == INVALID
     assert lib.lift_debug_set_grid_limit(0) == OK
 
