@@ -393,6 +393,8 @@ def run_lift(args):
             "clocks": sampler.summary(t_wall0, max(t_wall1, t_wall2)) if sampler else None,
             "e2e": e2e,
         }
+        if not args.no_extras:
+            line["next_rows"] = next_rows(lift, gen, torch, dev, stream, x_v, y_v, r_asum, ws_a)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_budget)
         print(json.dumps(line), flush=True)
@@ -402,6 +404,35 @@ def run_lift(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def next_rows(lift, gen, torch, dev, stream, x_v, y_v, r, ws, reps=20):
+    """NEXT rows measured beside the step (not part of it): the fused scal+asum (NEXT-2)
+    on the step's x, and BlackScholes on the paper's 4M prices (NEXT-3)."""
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(reps):
+            fn()
+        e.record(stream)
+        e.synchronize()
+        return s.elapsed_time(e) / reps * 1e3  # us
+    n = x_v.numel()
+    us_f = timed(lambda: lift.scal_asum(ALPHA_SCAL, x_v, out=y_v, result=r, ws=ws))
+    nb = 4 * 1024 * 1024
+    sp = gen.fill_device(torch.empty(nb, dtype=torch.float32, device=dev), 0, gen.TID_X, 0,
+                         gen.DIST_UNIFORM, 10.0, 200.0)
+    cp = torch.empty_like(sp)
+    pp = torch.empty_like(sp)
+    us_b = timed(lambda: lift.blackscholes(sp, 100.0, 0.05, 0.2, 1.0, call=cp, put=pp))
+    return {
+        "scal_asum_fused": {"n": n, "us": round(us_f, 2), "GB/s": round(8 * n / us_f / 1e3, 1),
+                            "vs_separate_scal_then_asum_bytes": "8 vs 12 B/element"},
+        "blackscholes": {"n": nb, "us": round(us_b, 2), "Goptions/s": round(nb / us_b / 1e3, 2),
+                         "GB/s": round(12 * nb / us_b / 1e3, 1), "bound": "alu (issue)"},
+    }
 
 
 def run_e2e(args, lift, ldist, gen, torch, dist, world, rank, dev, group, stream,
@@ -525,6 +556,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row timings")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "lift":
         print("note: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
