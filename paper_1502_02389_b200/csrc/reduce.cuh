@@ -112,6 +112,7 @@ struct ReduceArgs {
     int p, rank;
     unsigned long long epoch;  // > 0, increasing per call on the same buffers
     int* error;                // set to 1 if the peers did not arrive in time
+    int64_t prefetch_ahead;    // chunks between a CTA and the one it prefetches (0: off)
 };
 
 // ---- NEXT-1: the outermost reduce across GPUs, inside the kernel -------------------
@@ -241,6 +242,17 @@ __device__ __forceinline__ void chunk_body_tail(const float* xc, const float* yc
 // Resident CTAs per SM the register budget must allow (ptxas trades registers for how
 // many loads it issues up front).  Measured: asum 6 (all 4 loads up front, 40 regs),
 // dot 4 (all 8 loads up front); minBlocks 1 collapses occupancy (-40%).
+#ifdef LIFT_TRACE
+// Diagnostic builds only (-DLIFT_TRACE; never the product .so): per-chunk CTA
+// [start, end] globaltimer stamps and SM id, read back with lift_trace_read().
+__device__ unsigned long long g_trace[3 * 65536];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <class Op, int LW, int B>
 __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
@@ -248,6 +260,25 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
     int parity = 0;
 
     for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x, parity ^= 1) {
+#ifdef LIFT_TRACE
+        if (t == 0 && c < 65536) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_trace[3 * c] = gtimer();
+            g_trace[3 * c + 2] = smid;
+        }
+#endif
+        // Wave-ahead prefetch: the CTA that will start about one wave later (chunk
+        // c + prefetch_ahead, ~the resident CTA count) gets its chunk pulled into L2 by
+        // one TMA bulk prefetch now, so DRAM keeps streaming across wave boundaries
+        // instead of draining while each wave's CTAs finish and the next ones launch.
+        if (a.prefetch_ahead > 0 && t == 0) {
+            const int64_t pc = c + a.prefetch_ahead;
+            if (pc < a.nc && (pc + 1) * RED_C <= a.n) {
+                bulk_prefetch_l2(a.x + pc * RED_C, (uint32_t)(RED_C * 4));
+                if constexpr (Op::kTwoInputs) bulk_prefetch_l2(a.y + pc * RED_C, (uint32_t)(RED_C * 4));
+            }
+        }
         // ---- R1/R2: fused per-lane fold over the chunk ---------------------------
         const int64_t base = c * RED_C;
         const float* xc = a.x + base;
@@ -291,6 +322,9 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
                 __syncthreads();
             }
         }
+#ifdef LIFT_TRACE
+        if (t == 0 && c < 65536) g_trace[3 * c + 1] = gtimer();
+#endif
         if (warp != 0) continue;
 
         // ---- R4, warp 0 only: publish the chunk partial, group ticket ------------

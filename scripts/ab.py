@@ -38,6 +38,14 @@ def child(reps=30):
     bs_s = fill(4 << 20, 1, 10.0, 200.0)
     bs_c = torch.empty(4 << 20, dtype=torch.float32, device=dev)
     bs_p = torch.empty(4 << 20, dtype=torch.float32, device=dev)
+    def rot(f, k=4):
+        state = [0]
+
+        def g():
+            f(state[0] % k)
+            state[0] += 1
+        return g
+
     ops = {
         "scal_2p28": (lambda: lift.scal(3.0, x, out=y), 8 << 28),
         "asum_2p28": (lambda: lift.asum(x, out=r, ws=ws), 4 << 28),
@@ -46,6 +54,12 @@ def child(reps=30):
         "gemv_8192x16384": (lambda: lift.gemv(A2, gx2, gy, 1.5, 0.5, out=go),
                             4 * (8192 * 16384 + 16384 + 2 * 8192)),
         "asum_2p20": (lambda: lift.asum(x[:1 << 20], out=r, ws=ws), 4 << 20),
+        # mid sizes: rotate over 4 disjoint slices so no launch finds its data in L2
+        "asum_2p24": (rot(lambda i: lift.asum(x[i << 26:(i << 26) + (1 << 24)], out=r, ws=ws)),
+                      4 << 24),
+        "dot_2p24": (rot(lambda i: lift.dot(x[i << 26:(i << 26) + (1 << 24)],
+                                            y[i << 26:(i << 26) + (1 << 24)], out=r, ws=ws)),
+                     8 << 24),
         "scal_asum_2p28": (lambda: lift.scal_asum(3.0, x, out=y, result=r, ws=ws), 8 << 28),
         "bs_4M": (lambda: lift.blackscholes(bs_s, 100.0, 0.05, 0.2, 1.0, call=bs_c, put=bs_p),
                   12 * (4 << 20)),

@@ -1,0 +1,45 @@
+"""Diagnostic: CTA timeline of one asum launch (needs build/liblift_trace.so, -DLIFT_TRACE)."""
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["LIFT_LIB"] = os.path.join(ROOT, "build", "liblift_trace.so")
+import torch  # noqa: E402
+
+import lift_inputs as gen  # noqa: E402
+import paper_1502_02389_b200 as lift  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 24
+x = gen.fill_device(torch.empty(n, device="cuda"), 0, 1, 0, 0, -1.0, 1.0)
+ws = lift.Workspace(n, torch.device("cuda"))
+r = torch.empty(1, device="cuda")
+flush = torch.ones(128 << 20, device="cuda")
+for _ in range(3):
+    lift.asum(x, out=r, ws=ws)
+flush.sum()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record()
+lift.asum(x, out=r, ws=ws)
+e1.record()
+torch.cuda.synchronize()
+nc = (n + lift.CHUNK_ELEMS - 1) // lift.CHUNK_ELEMS
+buf = np.zeros(3 * 65536, np.uint64)
+lift._lib.lib.lift_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+lift._lib.lib.lift_trace_read(buf.ctypes.data, buf.nbytes)
+tr = buf[:3 * nc].reshape(nc, 3).astype(np.int64)
+t0 = tr[:, 0].min()
+start, end, sm = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, tr[:, 2]
+out = {"n": n, "event_us": e0.elapsed_time(e1) * 1e3, "chunks": nc,
+       "first_start_us": 0.0, "last_start_us": float(start.max()),
+       "last_end_us": float(end.max()), "median_cta_us": float(np.median(end - start)),
+       "p10_cta_us": float(np.percentile(end - start, 10)),
+       "p90_cta_us": float(np.percentile(end - start, 90)),
+       "sms_used": int(len(np.unique(sm))),
+       "start_quantiles_us": [float(np.percentile(start, q)) for q in (1, 10, 50, 90, 99)],
+       "end_quantiles_us": [float(np.percentile(end, q)) for q in (1, 10, 50, 90, 99)]}
+print(json.dumps(out, indent=1))

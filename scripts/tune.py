@@ -25,7 +25,8 @@ OUT = os.path.join(ROOT, "build", "tune")
 # (name, -D flags) — one axis at a time around the defaults, plus a few joint points
 SPACE = {
     "red_k": [("k2", "-DLIFT_RED_K=2"), ("k4", "-DLIFT_RED_K=4"),
-              ("k8", "-DLIFT_RED_K=8 -DLIFT_RED_G=128")],
+              ("k8", "-DLIFT_RED_K=8 -DLIFT_RED_G=128"),
+              ("k16", "-DLIFT_RED_K=16 -DLIFT_RED_G=64")],
     "asum_acc": [("asum_f32", "-DLIFT_ASUM_ACC=float"), ("asum_f64", "-DLIFT_ASUM_ACC=double")],
     "dot_acc": [("dot_f64", "-DLIFT_DOT_ACC=double"), ("dot_f32", "-DLIFT_DOT_ACC=float")],
     "gemv_ru": [("g_r1u8", "-DLIFT_GEMV_R=1 -DLIFT_GEMV_U=8"),
