@@ -223,13 +223,6 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
                              : (const void*)reduce_kernel<Op, 1, B>;
     const int64_t grid = grid_for(L.nc, fn, RED_T, 0, LIFT_PERSISTENT);
-#ifndef LIFT_RED_PREFETCH
-#define LIFT_RED_PREFETCH 1
-#endif
-    // prefetch one resident wave ahead (x, y must be 16-B aligned for the bulk prefetch)
-    a.prefetch_ahead = (LIFT_RED_PREFETCH && !LIFT_PERSISTENT && lw >= 4)
-                           ? (int64_t)sm_count(current_device()) * occupancy(fn, RED_T, 0)
-                           : 0;
     if (lw == 8) reduce_kernel<Op, 8, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
     else if (lw == 4) reduce_kernel<Op, 4, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
     else reduce_kernel<Op, 1, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);

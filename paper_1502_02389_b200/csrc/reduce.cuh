@@ -112,7 +112,6 @@ struct ReduceArgs {
     int p, rank;
     unsigned long long epoch;  // > 0, increasing per call on the same buffers
     int* error;                // set to 1 if the peers did not arrive in time
-    int64_t prefetch_ahead;    // chunks between a CTA and the one it prefetches (0: off)
 };
 
 // ---- NEXT-1: the outermost reduce across GPUs, inside the kernel -------------------
@@ -268,17 +267,6 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
             g_trace[3 * c + 2] = smid;
         }
 #endif
-        // Wave-ahead prefetch: the CTA that will start about one wave later (chunk
-        // c + prefetch_ahead, ~the resident CTA count) gets its chunk pulled into L2 by
-        // one TMA bulk prefetch now, so DRAM keeps streaming across wave boundaries
-        // instead of draining while each wave's CTAs finish and the next ones launch.
-        if (a.prefetch_ahead > 0 && t == 0) {
-            const int64_t pc = c + a.prefetch_ahead;
-            if (pc < a.nc && (pc + 1) * RED_C <= a.n) {
-                bulk_prefetch_l2(a.x + pc * RED_C, (uint32_t)(RED_C * 4));
-                if constexpr (Op::kTwoInputs) bulk_prefetch_l2(a.y + pc * RED_C, (uint32_t)(RED_C * 4));
-            }
-        }
         // ---- R1/R2: fused per-lane fold over the chunk ---------------------------
         const int64_t base = c * RED_C;
         const float* xc = a.x + base;
