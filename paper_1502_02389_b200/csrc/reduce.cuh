@@ -252,21 +252,120 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+// R3 + R4 for chunk c whose per-lane accumulators are `acc`: lane -> warp (butterfly)
+// -> CTA (8 warps pairwise) -> fp64 chunk partial; then warp 0 alone publishes it and
+// runs the two-level last-block-done.  Exactly one CTA barrier on the common path.
+template <class Op, int LW, int B>
+__device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
+                                             const typename Op::acc_t* acc, double (*wbuf)[8],
+                                             int parity) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t base = c * RED_C;
+    double lane8[RED_V];
+    bool bad = false;
+#pragma unroll
+    for (int e = 0; e < RED_V; ++e) {
+        lane8[e] = (double)acc[e];
+        if constexpr (sizeof(acc[0]) == 4) bad |= !isfinite(acc[e]);
+    }
+    double wv = warp_pairwise(pairwise8(lane8));
+    if (lane == 0) wbuf[parity][warp] = wv;
+    bool redo = false;
+    if constexpr (sizeof(acc[0]) == 4) redo = __syncthreads_or(bad);  // the one barrier
+    else __syncthreads();
+    if constexpr (sizeof(acc[0]) == 4) {
+        if (redo) {  // rare: an fp32 run overflowed (or the chunk holds Inf/NaN)
+            const float* xc = a.x + base;
+            const float* yc = Op::kTwoInputs ? a.y + base : nullptr;
+            const bool full = base + RED_C <= a.n;
+            double acc64[RED_V];
+#pragma unroll
+            for (int e = 0; e < RED_V; ++e) acc64[e] = 0.0;
+            if constexpr (Op::kMapStore) {
+                // refold this thread's own stored map values
+                chunk_body_tail<AsumOp<double>>(a.map_out + base, nullptr,
+                                                min((int64_t)RED_C, a.n - base), acc64);
+            } else {
+                using Op64 = typename Op::template rebind<double>;
+                if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64);
+                else chunk_body_tail<Op64>(xc, yc, a.n - base, acc64);
+            }
+            wv = warp_pairwise(pairwise8(acc64));
+            if (lane == 0) wbuf[parity][warp] = wv;  // nobody reads wbuf before the barrier
+            __syncthreads();
+        }
+    }
+#ifdef LIFT_TRACE
+    if (t == 0 && c < 65536) g_trace[3 * c + 1] = gtimer();
+#endif
+    if (warp != 0) return;
+
+    // ---- R4, warp 0 only: publish the chunk partial, group ticket ----------------
+    const int64_t g = c / RED_G;
+    unsigned last = 0;
+    if (lane == 0) {
+        a.chunk_part[c] = pairwise8(wbuf[parity]);
+        __threadfence();
+        const int64_t gcount = min((int64_t)RED_G, a.nc - g * RED_G);
+        last = (atomicAdd(&a.tick[g], 1u) == (unsigned)(gcount - 1));
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+
+    // Last chunk of group g: fold the group's RED_G chunk partials (pairwise).
+    __threadfence();
+    const int64_t g0 = g * RED_G;
+    const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
+    if (a.ng == 1) {  // one group: the pairwise fold over one leaf is the leaf itself
+        if (lane == 0) a.tick[0] = 0u;
+        if (a.peers) {
+            xchg_combine(a, gpart);
+        } else if (lane == 0) {
+            if (a.out_f64) *a.out_f64 = gpart;
+            if (a.out_f32) *a.out_f32 = __double2float_rn(gpart);
+        }
+        return;
+    }
+    last = 0;
+    if (lane == 0) {
+        a.group_part[g] = gpart;
+        a.tick[g] = 0u;  // reset for the next call (workspace contract)
+        __threadfence();
+        last = (atomicAdd(&a.tick[a.ng], 1u) == (unsigned)(a.ng - 1));
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+
+    // Last group: final pairwise fold over the group partials, round once.
+    __threadfence();
+    const double total = warp_fold_leaves(a.group_part, a.ng);
+    if (lane == 0) a.tick[a.ng] = 0u;
+    if (a.peers) {
+        xchg_combine(a, total);
+    } else if (lane == 0) {
+        if (a.out_f64) *a.out_f64 = total;
+        if (a.out_f32) *a.out_f32 = __double2float_rn(total);
+    }
+}
+
+__device__ __forceinline__ void trace_start(int64_t c) {
+#ifdef LIFT_TRACE
+    if (threadIdx.x == 0 && c < 65536) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace[3 * c] = gtimer();
+        g_trace[3 * c + 2] = smid;
+    }
+#else
+    (void)c;
+#endif
+}
+
+// One CTA per chunk, hardware-scheduled (the default).
 template <class Op, int LW, int B>
 __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     int parity = 0;
-
     for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x, parity ^= 1) {
-#ifdef LIFT_TRACE
-        if (t == 0 && c < 65536) {
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            g_trace[3 * c] = gtimer();
-            g_trace[3 * c + 2] = smid;
-        }
-#endif
+        trace_start(c);
         // ---- R1/R2: fused per-lane fold over the chunk ---------------------------
         const int64_t base = c * RED_C;
         const float* xc = a.x + base;
@@ -274,91 +373,10 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
         typename Op::acc_t acc[RED_V];
 #pragma unroll
         for (int e = 0; e < RED_V; ++e) acc[e] = 0;
-        const bool full = base + RED_C <= a.n;
         float* mo = Op::kMapStore ? a.map_out + base : nullptr;
-        if (full) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo);
+        if (base + RED_C <= a.n) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo);
         else chunk_body_tail<Op>(xc, yc, a.n - base, acc, a.alpha, mo);
-
-        // ---- R3: lane -> warp (butterfly) -> CTA (8 warps pairwise), fp64 --------
-        double lane8[RED_V];
-        bool bad = false;
-#pragma unroll
-        for (int e = 0; e < RED_V; ++e) {
-            lane8[e] = (double)acc[e];
-            if constexpr (sizeof(acc[0]) == 4) bad |= !isfinite(acc[e]);
-        }
-        double wv = warp_pairwise(pairwise8(lane8));
-        if (lane == 0) wbuf[parity][warp] = wv;
-        bool redo = false;
-        if constexpr (sizeof(acc[0]) == 4) redo = __syncthreads_or(bad);  // the one barrier
-        else __syncthreads();
-        if constexpr (sizeof(acc[0]) == 4) {
-            if (redo) {  // rare: an fp32 run overflowed (or the chunk holds Inf/NaN)
-                double acc64[RED_V];
-#pragma unroll
-                for (int e = 0; e < RED_V; ++e) acc64[e] = 0.0;
-                if constexpr (Op::kMapStore) {
-                    // refold this thread's own stored map values
-                    chunk_body_tail<AsumOp<double>>(mo, nullptr, min((int64_t)RED_C, a.n - base), acc64);
-                } else {
-                    using Op64 = typename Op::template rebind<double>;
-                    if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64);
-                    else chunk_body_tail<Op64>(xc, yc, a.n - base, acc64);
-                }
-                wv = warp_pairwise(pairwise8(acc64));
-                if (lane == 0) wbuf[parity][warp] = wv;  // nobody reads wbuf before the barrier
-                __syncthreads();
-            }
-        }
-#ifdef LIFT_TRACE
-        if (t == 0 && c < 65536) g_trace[3 * c + 1] = gtimer();
-#endif
-        if (warp != 0) continue;
-
-        // ---- R4, warp 0 only: publish the chunk partial, group ticket ------------
-        const int64_t g = c / RED_G;
-        unsigned last = 0;
-        if (lane == 0) {
-            a.chunk_part[c] = pairwise8(wbuf[parity]);
-            __threadfence();
-            const int64_t gcount = min((int64_t)RED_G, a.nc - g * RED_G);
-            last = (atomicAdd(&a.tick[g], 1u) == (unsigned)(gcount - 1));
-        }
-        if (!__shfl_sync(0xffffffffu, last, 0)) continue;
-
-        // Last chunk of group g: fold the group's RED_G chunk partials (pairwise).
-        __threadfence();
-        const int64_t g0 = g * RED_G;
-        const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
-        if (a.ng == 1) {  // one group: the pairwise fold over one leaf is the leaf itself
-            if (lane == 0) a.tick[0] = 0u;
-            if (a.peers) {
-                xchg_combine(a, gpart);
-            } else if (lane == 0) {
-                if (a.out_f64) *a.out_f64 = gpart;
-                if (a.out_f32) *a.out_f32 = __double2float_rn(gpart);
-            }
-            continue;
-        }
-        last = 0;
-        if (lane == 0) {
-            a.group_part[g] = gpart;
-            a.tick[g] = 0u;  // reset for the next call (workspace contract)
-            __threadfence();
-            last = (atomicAdd(&a.tick[a.ng], 1u) == (unsigned)(a.ng - 1));
-        }
-        if (!__shfl_sync(0xffffffffu, last, 0)) continue;
-
-        // Last group: final pairwise fold over the group partials, round once.
-        __threadfence();
-        const double total = warp_fold_leaves(a.group_part, a.ng);
-        if (lane == 0) a.tick[a.ng] = 0u;
-        if (a.peers) {
-            xchg_combine(a, total);
-        } else if (lane == 0) {
-            if (a.out_f64) *a.out_f64 = total;
-            if (a.out_f32) *a.out_f32 = __double2float_rn(total);
-        }
+        chunk_finish<Op, LW, B>(a, c, acc, wbuf, parity);
     }
 }
 
