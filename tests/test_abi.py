@@ -147,3 +147,26 @@ def test_product_never_imports_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace(
                     "no oracle", ""), f"{f} references the oracle"
+
+
+def _build_c_example(out):
+    cmd = ["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+           "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "lift_c_example.c"),
+           "-L", os.path.join(ROOT, "paper_1502_02389_b200"), "-llift",
+           "-L", "/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath," + os.path.join(ROOT, "paper_1502_02389_b200"), "-o", out]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def test_c_example_builds_against_the_header(tmp_path):
+    """The boundary is usable from plain C: the example compiles and links (runs on GPU)."""
+    r = _build_c_example(str(tmp_path / "lift_c_example"))
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    exe = str(tmp_path / "lift_c_example")
+    assert _build_c_example(exe).returncode == 0
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
