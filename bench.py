@@ -379,8 +379,9 @@ def run_lift(args):
                                    "n=2^26 (configs[1]) + gemv 8192x8192 a=1.5 b=0.5 "
                                    "(configs[3]), per rank",
                        "global_batch": world, "parallelism": f"shard{world} (weak)",
-                       "x1": {"none": "single GPU", "fused": "asum/dot combine fused into the "
-                              "reduction kernel over peer memory; gemv y all-gather (NCCL)",
+                       "x1": {"none": "single GPU", "fused": "asum/dot combine and the gemv y "
+                              "all-gather fused into the kernels over peer memory (no NCCL "
+                              "launch in the step)",
                               "nccl": "all-gather + lift_combine; gemv y all-gather"}[x1_mode],
                        "l2": "no flush: every operand >= 256 MiB > 126 MB L2",
                        "frac_of_8TBs": round(value / world / NOMINAL_HBM, 4)},
