@@ -432,7 +432,7 @@ def next_rows(lift, gen, torch, dev, stream, x_v, y_v, r, ws, reps=20):
         "scal_asum_fused": {"n": n, "us": round(us_f, 2), "GB/s": round(8 * n / us_f / 1e3, 1),
                             "vs_separate_scal_then_asum_bytes": "8 vs 12 B/element"},
         "blackscholes": {"n": nb, "us": round(us_b, 2), "Goptions/s": round(nb / us_b / 1e3, 2),
-                         "GB/s": round(12 * nb / us_b / 1e3, 1), "bound": "alu (issue)"},
+                         "GB/s": round(12 * nb / us_b / 1e3, 1), "bound": "memory (48 MB in+out: fits the 126 MB L2 across repeats)"},
     }
 
 

@@ -539,7 +539,10 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
     const int64_t body = n - head;
     const int64_t nslots = body / 8;
     const int tail = (int)(body % 8);
-    const BsParams p{K, r, v, T};
+    const double vs = (double)v * sqrt((double)T);
+    const BsConst p{(float)(M_LN2 / vs),
+                    (float)((((double)r + 0.5 * (double)v * v) * T - log((double)K)) / vs),
+                    (float)vs, (float)(K * exp(-(double)r * T))};
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t tile = (int64_t)BS_T * BS_U;
     if (same) {

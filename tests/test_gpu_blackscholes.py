@@ -75,3 +75,15 @@ def test_blackscholes_alignment_and_empty(lift):
     e = torch.empty(0, device=DEV)
     c, p = lift.blackscholes(e, K, R, V, T)
     assert c.numel() == 0 and p.numel() == 0
+
+
+def test_blackscholes_extreme_moneyness(lift):
+    """Deep in/out of the money and s = 0 (d = -inf): finite, within the bar, and the
+    limits call -> max(s - K e^{-rT}, 0), put -> max(K e^{-rT} - s, 0) hold."""
+    s = np.array([0.0, 1e-30, 1e-3, 1.0, 1e4, 1e6, 3e7], dtype=np.float32)
+    c, p = (t.cpu().numpy() for t in lift.blackscholes(torch.from_numpy(s).to(DEV), K, R, V, T))
+    assert np.all(np.isfinite(c)) and np.all(np.isfinite(p))
+    oc, op = oracle.blackscholes(s, K, R, V, T)
+    scale = s.astype(np.float64) + K
+    assert (np.abs(c - oc) / scale).max() <= 1e-6 and (np.abs(p - op) / scale).max() <= 1e-6
+    assert c[0] == 0.0 and abs(p[0] - K * np.exp(-R * T)) <= 1e-4
