@@ -147,8 +147,42 @@ def oracle_step(s):
     oracle.gemv(s["A"], s["gx"], s["gy"], ALPHA, BETA)
 
 
-def cpu_baseline(budget_s: float = 10.0, frac_shift: int = 3):
-    """The oracle as it stands, single-threaded, on a bounded sample (rank 0, N=1)."""
+def oracle_step_cores(s, pool, k):
+    """The same oracle functions run concurrently on k contiguous shards of every operand
+    (fixed 2^16-element-aligned boundaries, partials combined in shard order; the ctypes
+    calls release the GIL).  Timing only: SURVEY §8(d) asks for the oracle on all cores."""
+    import oracle
+
+    def cuts(n):
+        g = 1 << 16
+        step = max(g, (n + k * g - 1) // (k * g) * g)  # ceil(n / k), rounded up to 2^16
+        return [(a, min(n, a + step)) for a in range(0, n, step)]
+    jobs = [pool.submit(oracle.scal, ALPHA_SCAL, s["x"][a:b]) for a, b in cuts(len(s["x"]))]
+    jobs += [pool.submit(oracle.asum, s["x"][a:b]) for a, b in cuts(len(s["x"]))]
+    jobs += [pool.submit(oracle.dot, s["dx"][a:b], s["dy"][a:b]) for a, b in cuts(len(s["dx"]))]
+    m = s["A"].shape[0]
+    rows = max(1, -(-m // k))
+    jobs += [pool.submit(oracle.gemv, s["A"][a:a + rows], s["gx"], s["gy"][a:a + rows], ALPHA, BETA)
+             for a in range(0, m, rows)]
+    for j in jobs:
+        j.result()
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(budget_s: float = 10.0, frac_shift: int = 3, cores_budget_s: float = 5.0):
+    """The oracle as it stands, single-threaded, on a bounded sample (rank 0, N=1); plus the
+    same oracle run over all host cores under "all_cores"."""
+    from concurrent.futures import ThreadPoolExecutor
     s = oracle_sample(frac_shift)
     oracle_step(s)  # warm
     reps, t0 = 0, time.perf_counter()
@@ -158,9 +192,24 @@ def cpu_baseline(budget_s: float = 10.0, frac_shift: int = 3):
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": round(s["bytes"] * reps / dt / 1e9, 3), "unit": "GB/s", "cores": 1,
-            "kind": "oracle",
-            "sample": f"{reps} x ({s['desc']}) in {dt:.1f} s, fp64 Neumaier C oracle, 1 thread"}
+    out = {"value": round(s["bytes"] * reps / dt / 1e9, 3), "unit": "GB/s", "cores": 1,
+           "kind": "oracle",
+           "sample": f"{reps} x ({s['desc']}) in {dt:.1f} s, fp64 Neumaier C oracle, 1 thread"}
+    k = len(os.sched_getaffinity(0))
+    with ThreadPoolExecutor(k) as pool:
+        oracle_step_cores(s, pool, k)  # warm
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            oracle_step_cores(s, pool, k)
+            reps += 1
+            if time.perf_counter() - t0 >= cores_budget_s:
+                break
+        dt = time.perf_counter() - t0
+    out["host_cpu"] = _cpu_model()
+    out["all_cores"] = {"value": round(s["bytes"] * reps / dt / 1e9, 3), "unit": "GB/s",
+                        "cores": k, "sample": f"{reps} x (same step, every operand in {k} "
+                        f"shards on {k} threads) in {dt:.1f} s"}
+    return out
 
 
 def run_reference(args):
