@@ -15,6 +15,7 @@ fallback: a CPU tensor is an error, and a missing liblift.so fails at import.
 """
 from __future__ import annotations
 
+import os
 import threading
 
 import torch
@@ -44,8 +45,15 @@ def _vec(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
+#: Debug aid for tests: allocate results pre-filled with NaN, so that an element a kernel
+#: fails to write cannot pass by inheriting a correct value from a recycled allocation.
+POISON_OUTPUTS = os.environ.get("LIFT_POISON_OUTPUTS", "") not in ("", "0")
+
+
 def _out(out, n, dtype, device, name="out"):
     if out is None:
+        if POISON_OUTPUTS:
+            return torch.full((n,), float("nan"), dtype=dtype, device=device)
         return torch.empty(n, dtype=dtype, device=device)
     if (not out.is_cuda or out.dtype != dtype or out.numel() != n or not out.is_contiguous()
             or out.device != device):

@@ -208,6 +208,10 @@ __device__ __forceinline__ bool clc_fetch(Clc& c, int64_t& next) {
         : "r"(smem_u32(c.resp))
         : "memory");
     next = cx;
+#ifndef LIFT_CLC_NOFENCE
+    // order this generic read of the response before the next try_cancel's async write
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     return ok != 0;
 }
 

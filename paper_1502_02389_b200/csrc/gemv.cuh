@@ -50,7 +50,10 @@ namespace lift {
 constexpr int GEMV_R = LIFT_GEMV_R;
 constexpr int GEMV_U = LIFT_GEMV_U;
 constexpr int GEMV_PMAX = 16384;             // max x-panel columns staged in shared memory
-constexpr int GEMV_XSTG = 4096;              // fp32 staging buffer (floats) for the bulk copy
+#ifndef LIFT_GEMV_XSTG
+#define LIFT_GEMV_XSTG 4096
+#endif
+constexpr int GEMV_XSTG = LIFT_GEMV_XSTG;     // fp32 staging buffer (floats) for the bulk copy
 constexpr int GEMV_SMEM_LIMIT = 227 * 1024;  // opt-in dynamic shared memory per CTA
 
 struct GemvArgs {
@@ -242,7 +245,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) gemv_kernel(GemvArgs 
     constexpr int64_t rows_per_block = (int64_t)(NT / 32) * R;
     int64_t blk = blockIdx.x;
     while (true) {
+#ifndef LIFT_GEMV_NOCLC
         if (threadIdx.x == 0) clc_try_cancel(clc);  // steal the next block while we work
+#endif
         const int64_t r0 = blk * rows_per_block + (int64_t)warp * R;
         int64_t rows[R];
 #pragma unroll
@@ -264,7 +269,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) gemv_kernel(GemvArgs 
         }
         if (r0 < a.m) gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
         int64_t next;
+#ifndef LIFT_GEMV_NOCLC
         const bool more = clc_fetch(clc, next);
+#else
+        const bool more = false;
+        next = 0;
+#endif
         __syncthreads();  // everyone has read the response before it is reused
         if (a.y_peers && warp == 0) gemv_block_done(a);  // after the barrier: rows stored
         if (!more) break;

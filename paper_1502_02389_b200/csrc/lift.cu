@@ -240,26 +240,42 @@ const void* scal_fn(bool alias) {
     return alias ? (const void*)scal_kernel<LW, true> : (const void*)scal_kernel<LW, false>;
 }
 
-template <int NT, int LW, bool MULTI>
+#ifndef LIFT_GEMV_SMALL
+#define LIFT_GEMV_SMALL 1  // short-m path (fewer rows per block); 0 disables
+#endif
+#ifndef LIFT_GEMV_SMALL_ROWS_PER_SM
+#define LIFT_GEMV_SMALL_ROWS_PER_SM 24  // use it when m < this x SMs (1.5 default blocks per SM)
+#endif
+#ifndef LIFT_GEMV_SNT
+#define LIFT_GEMV_SNT 256
+#endif
+#ifndef LIFT_GEMV_SR
+#define LIFT_GEMV_SR 1
+#endif
+#ifndef LIFT_GEMV_SU
+#define LIFT_GEMV_SU 8
+#endif
+
+template <int NT, int R, int U, int LW, bool MULTI>
 lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
     const size_t smem = gemv_smem_bytes(a.P);
-    const void* fn = (const void*)gemv_kernel<NT, GEMV_R, GEMV_U, LW, MULTI>;
-    const int64_t rows_per_cta = (int64_t)(NT / 32) * GEMV_R;
+    const void* fn = (const void*)gemv_kernel<NT, R, U, LW, MULTI>;
+    const int64_t rows_per_cta = (int64_t)(NT / 32) * R;
     const int64_t blocks = (a.m + rows_per_cta - 1) / rows_per_cta;
     const int64_t grid = grid_for(blocks, fn, NT, smem, false, true);  // CLC steals the rest
     GemvArgs b = a;
     b.nblocks = blocks;
-    gemv_kernel<NT, GEMV_R, GEMV_U, LW, MULTI><<<(unsigned)grid, NT, smem, s>>>(b);
+    gemv_kernel<NT, R, U, LW, MULTI><<<(unsigned)grid, NT, smem, s>>>(b);
     return launched();
 }
 
-template <int NT>
+template <int NT, int R, int U>
 lift_status gemv_pick(const GemvArgs& a, int lw, bool multi, cudaStream_t s) {
     if (multi)
-        return lw == 8 ? gemv_go<NT, 8, true>(a, s) : lw == 4 ? gemv_go<NT, 4, true>(a, s)
-                                                             : gemv_go<NT, 1, true>(a, s);
-    return lw == 8 ? gemv_go<NT, 8, false>(a, s) : lw == 4 ? gemv_go<NT, 4, false>(a, s)
-                                                          : gemv_go<NT, 1, false>(a, s);
+        return lw == 8 ? gemv_go<NT, R, U, 8, true>(a, s) : lw == 4 ? gemv_go<NT, R, U, 4, true>(a, s)
+                                                                   : gemv_go<NT, R, U, 1, true>(a, s);
+    return lw == 8 ? gemv_go<NT, R, U, 8, false>(a, s) : lw == 4 ? gemv_go<NT, R, U, 4, false>(a, s)
+                                                                : gemv_go<NT, R, U, 1, false>(a, s);
 }
 
 lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
@@ -268,10 +284,20 @@ lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
     a.xs_stride = a.P / 8 + 1;
     const uintptr_t aa = reinterpret_cast<uintptr_t>(a.A);
     const int lw = ((aa & 31) == 0 && a.lda % 8 == 0) ? 8 : ((aa & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
+    const bool two = 2 * gemv_smem_bytes(a.P) <= (size_t)GEMV_SMEM_LIMIT;
+#if LIFT_GEMV_SMALL
+    // Short m: the default 16-row blocks would leave SMs without a CTA (m = 1024 -> 64
+    // blocks on 148 SMs).  One row per warp (8-row blocks) with 8 k-steps of loads in
+    // flight instead (measured, scripts/ab_gemv.py: 1024x8192 14.3 -> 10.9 us, 2048x8192
+    // 16.4 -> 14.7 us); every (NT, R, U) gives the same bits (each row's order is fixed
+    // by the lane/slot map).
+    if (two && a.m < (int64_t)LIFT_GEMV_SMALL_ROWS_PER_SM * sm_count(current_device()))
+        return gemv_pick<LIFT_GEMV_SNT, LIFT_GEMV_SR, LIFT_GEMV_SU>(a, lw, multi, s);
+#endif
     // Two 256-thread CTAs per SM while x fits twice in shared memory; otherwise one
     // 512-thread CTA, so an SM always runs 16 warps.
-    if (2 * gemv_smem_bytes(a.P) <= (size_t)GEMV_SMEM_LIMIT) return gemv_pick<256>(a, lw, multi, s);
-    return gemv_pick<512>(a, lw, multi, s);
+    if (two) return gemv_pick<256, GEMV_R, GEMV_U>(a, lw, multi, s);
+    return gemv_pick<512, GEMV_R, GEMV_U>(a, lw, multi, s);
 }
 
 }  // namespace

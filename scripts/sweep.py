@@ -27,36 +27,85 @@ def fill(n, tid, lo, hi):
 flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)
 
 
+flush_out = torch.empty((), dtype=torch.float32, device=dev)
+
+
+def _flush():
+    torch.sum(flush, dim=0, out=flush_out)
+
+
+def _graph(s, fns):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for f in fns:
+            f()
+    return g
+
+
+def _replay_ms(g, s):
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record(s)
+    g.replay()
+    e1.record(s)
+    e1.synchronize()
+    return e0.elapsed_time(e1)
+
+
 def time_op(fn, nbytes, reps=20, flush_l2=True):
-    """Median over `reps` of one graph-replayed launch; L2 flushed (by reads) before each.
-    A single launch includes its ramp-up and drain, so these are lower than the
-    back-to-back figures of scripts/ab.py and bench.py."""
+    """One graph-replayed launch, L2 flushed (by reads) before each; A single launch
+    includes its ramp-up and drain, so these are lower than the back-to-back figures of
+    scripts/ab.py and bench.py.
+      us / p10 / p90: per-launch CUDA events (median, 10th, 90th percentile of `reps`);
+                      the event timestamps are coarse (~2 us steps on this box);
+      us_diff:        (graph of reps x [flush, op]) - (graph of reps x [flush]), / reps —
+                      the same launch without the timestamp granularity."""
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
         fn()  # warm (workspace, occupancy cache)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            fn()
-    ts = []
-    for _ in range(reps):
+        g = _graph(s, [fn])
+        ts = []
+        for _ in range(reps):
+            if flush_l2:
+                _flush()
+            ts.append(_replay_ms(g, s))
+        ts.sort()
+        res = {}
         if flush_l2:
-            flush.sum()
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record()
-        g.replay()
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    ts.sort()
+            g1 = _graph(s, [f for _ in range(reps) for f in (_flush, fn)])
+            g0 = _graph(s, [_flush] * reps)
+            d1, d0 = [], []
+            for _ in range(5):
+                d1.append(_replay_ms(g1, s))
+                d0.append(_replay_ms(g0, s))
+            d1.sort()
+            d0.sort()
+            res["us_diff"] = round((d1[2] - d0[2]) / reps * 1e3, 2)
     us = ts[len(ts) // 2] * 1e3
     gbs = nbytes / (us * 1e-6) / 1e9
-    return {"us": round(us, 2), "GB/s": round(gbs, 1), "frac_measured": round(gbs / PEAK, 3),
-            "frac_8TBs": round(gbs / 8000, 3)}
+    out = {"us": round(us, 2), "p10": round(ts[len(ts) // 10] * 1e3, 2),
+           "p90": round(ts[(9 * len(ts)) // 10] * 1e3, 2), **res,
+           "GB/s": round(gbs, 1), "frac_measured": round(gbs / PEAK, 3),
+           "frac_8TBs": round(gbs / 8000, 3)}
+    if "us_diff" in res and res["us_diff"] > 0:
+        out["GB/s_diff"] = round(nbytes / (res["us_diff"] * 1e-6) / 1e9, 1)
+    return out
+
+
+def time_b2b(fn, nbytes, reps=50):
+    """L2-warm, back-to-back: `reps` launches in one graph, no flush (labelled as such)."""
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        g = _graph(s, [fn] * reps)
+        t = sorted(_replay_ms(g, s) for _ in range(5))[2] / reps * 1e3
+    return {"us": round(t, 2), "GB/s": round(nbytes / (t * 1e-6) / 1e9, 1), "l2": "warm"}
 
 
 out = {"note": "device time per launch, CUDA graph replay, L2 flushed before each launch, "
-               "median of 20; HBM roofline denominators: 6451.8 GB/s measured, 8 TB/s nominal"}
+               "median of 20 (p10/p90; us_diff = graph-difference timing, see time_op); "
+               "*_b2b: L2-warm back-to-back graph replays; HBM roofline denominators: 6451.8 GB/s measured, 8 TB/s nominal"}
 x = fill(1 << 28, 1, -1.0, 1.0)
 y = fill(1 << 28, 2, 0.0, 2.0)
 yo = torch.empty(1 << 28, dtype=torch.float32, device=dev)
@@ -83,4 +132,14 @@ for (m, n) in [(4096, 4096), (8192, 8192), (8192, 16384)]:
     out[f"gemv_{m}x{n}"] = time_op(lambda: lift.gemv(A, gx, gy, 1.5, 0.5, out=go),
                                    4 * (m * n + n + 2 * m))
     del A
+# L2-warm back-to-back figures for C1 and for C4's per-rank shard at p = 8
+xs = fill(1 << 20, 1, 0.0, 1.0)
+out["asum_2^20_b2b"] = time_b2b(lambda: lift.asum(xs, out=r, ws=ws), 4 << 20)
+A = fill(1024 * 8192, 3, 0.0, 3.0).view(1024, 8192)
+gx, gy = fill(8192, 1, 0.0, 1.0), fill(1024, 2, 0.0, 2.0)
+go = torch.empty(1024, dtype=torch.float32, device=dev)
+out["gemv_1024x8192_p8shard_b2b"] = time_b2b(lambda: lift.gemv(A, gx, gy, 1.5, 0.5, out=go),
+                                             4 * (1024 * 8192 + 8192 + 2 * 1024))
+out["gemv_1024x8192_p8shard"] = time_op(lambda: lift.gemv(A, gx, gy, 1.5, 0.5, out=go),
+                                        4 * (1024 * 8192 + 8192 + 2 * 1024))
 print(json.dumps(out, indent=1))
