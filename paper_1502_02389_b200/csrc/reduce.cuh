@@ -160,17 +160,34 @@ __device__ __forceinline__ double warp_fold_leaves(const double* leaves, int64_t
     int64_t p2 = 1;
     while (p2 < nleaf) p2 <<= 1;
     const int64_t blk = p2 > 32 ? p2 / 32 : 1;
+    const int64_t l0 = (int64_t)lane * blk;
     double v;
     if (blk == 1) {
         v = (lane < nleaf) ? __ldcg(leaves + lane) : 0.0;
+    } else if (blk <= 8) {
+        // all of the lane's leaves in flight at once (one L2 round trip), then the
+        // pairwise tree over them
+        double w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = (i < blk && l0 + i < nleaf) ? __ldcg(leaves + l0 + i) : 0.0;
+        if (blk == 2) v = __dadd_rn(w[0], w[1]);
+        else if (blk == 4) v = __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3]));
+        else v = pairwise8(w);
     } else {
+        // batches of 8 leaves (8 loads in flight), each batch's subtree pushed on a
+        // binary-counter stack: the pairwise tree over aligned batches of 8 leaves
         double stk[40];
         int top = 0;
-        for (int64_t i = 0; i < blk; ++i) {
-            const int64_t li = (int64_t)lane * blk + i;
-            double w = (li < nleaf) ? __ldcg(leaves + li) : 0.0;
-            for (int64_t cnt = i; cnt & 1; cnt >>= 1) w = __dadd_rn(stk[--top], w);
-            stk[top++] = w;
+        for (int64_t b = 0; b < blk / 8; ++b) {
+            double w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int64_t li = l0 + 8 * b + i;
+                w[i] = (li < nleaf) ? __ldcg(leaves + li) : 0.0;
+            }
+            double s = pairwise8(w);
+            for (int64_t cnt = b; cnt & 1; cnt >>= 1) s = __dadd_rn(stk[--top], s);
+            stk[top++] = s;
         }
         v = stk[0];
     }
