@@ -39,6 +39,10 @@
 
 namespace lift {
 
+#ifndef LIFT_SC_FENCE
+#define LIFT_SC_FENCE 0
+#endif
+
 // The fused per-element step (rule 5f).  Acc is the per-lane accumulator type.
 //  * asum uses fp32 accumulators over its RED_K = 4-term runs (|x| is exact, so only
 //    4-term rounding) — no fp32->fp64 conversion per element.  A run can only
@@ -148,6 +152,29 @@ __device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) 
         if (a.out_f64) *a.out_f64 = r;
         if (a.out_f32) *a.out_f32 = __double2float_rn(r);
     }
+}
+
+// Last-block-done tickets.  Lane 0 publishes a partial with a plain store and takes a
+// ticket with an acq_rel atomic (release: its store before the ticket; acquire: every
+// earlier ticket holder's store before what follows); the warp barrier then orders the
+// other lanes' leaf loads after lane 0's acquire.  (LIFT_SC_FENCE: the __threadfence
+// pair instead, for A/B runs.)
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
+#if LIFT_SC_FENCE
+    __threadfence();
+    return atomicAdd(t, 1u);
+#else
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    return old;
+#endif
+}
+__device__ __forceinline__ void ticket_acquired() {
+#if LIFT_SC_FENCE
+    __threadfence();
+#else
+    __syncwarp();
+#endif
 }
 
 // Warp-level pairwise fold of `nleaf` fp64 leaves read from global memory (L2),
@@ -322,14 +349,13 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
     unsigned last = 0;
     if (lane == 0) {
         a.chunk_part[c] = pairwise8(wbuf[parity]);
-        __threadfence();
         const int64_t gcount = min((int64_t)RED_G, a.nc - g * RED_G);
-        last = (atomicAdd(&a.tick[g], 1u) == (unsigned)(gcount - 1));
+        last = (ticket_acq_rel(&a.tick[g]) == (unsigned)(gcount - 1));
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
 
     // Last chunk of group g: fold the group's RED_G chunk partials (pairwise).
-    __threadfence();
+    ticket_acquired();
     const int64_t g0 = g * RED_G;
     const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
     if (a.ng == 1) {  // one group: the pairwise fold over one leaf is the leaf itself
@@ -346,13 +372,12 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
     if (lane == 0) {
         a.group_part[g] = gpart;
         a.tick[g] = 0u;  // reset for the next call (workspace contract)
-        __threadfence();
-        last = (atomicAdd(&a.tick[a.ng], 1u) == (unsigned)(a.ng - 1));
+        last = (ticket_acq_rel(&a.tick[a.ng]) == (unsigned)(a.ng - 1));
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
 
     // Last group: final pairwise fold over the group partials, round once.
-    __threadfence();
+    ticket_acquired();
     const double total = warp_fold_leaves(a.group_part, a.ng);
     if (lane == 0) a.tick[a.ng] = 0u;
     if (a.peers) {
