@@ -102,6 +102,8 @@ template <int LW>
 __global__ void __launch_bounds__(BS_T) blackscholes_kernel(int64_t nslots, int head, int tail,
                                                             const float* s, float* call,
                                                             float* put, BsConst c) {
+    pdl_wait();
+    pdl_trigger();
     const int t = threadIdx.x;
     if (blockIdx.x == 0) {
         const int64_t tb = head + 8 * nslots;

@@ -97,6 +97,19 @@ __device__ __forceinline__ double warp_pairwise(double v) {
     return v;
 }
 
+// ---- Programmatic dependent launch (sm_90+) ------------------------------------------
+// Every lift kernel is launched with programmatic stream serialization (lift.cu,
+// launch()), so its CTAs may be scheduled while the previous kernel on the stream still
+// drains.  pdl_wait() blocks until that kernel has completed and its memory is visible;
+// it is the first statement of every kernel, before any global access, which makes the
+// early start safe whatever the previous kernel was (a no-op when launched without the
+// attribute).  pdl_trigger() lets the NEXT kernel's CTAs be scheduled once every CTA of
+// this one has started (they then wait in their own pdl_wait()).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---- mbarrier + TMA bulk copy (cp.async.bulk -> SASS UBLKCP) -------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -226,6 +226,8 @@ template <int NT, int R, int U, int LW, bool MULTI>
 // minBlocks = 2 for 256 threads (two CTAs per SM) gives ptxas a 128-register budget, which
 // it spends on issuing all GEMV_U x GEMV_R 256-bit loads of a step up front (measured).
 __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) gemv_kernel(GemvArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint64_t* clc_bar = reinterpret_cast<uint64_t*>(smem + 8);

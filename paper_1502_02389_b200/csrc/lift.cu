@@ -34,6 +34,8 @@ namespace lift {
 
 // X1: outermost reduce over p per-rank fp64 partials, pairwise (zero-padded to 2^k).
 __global__ void combine_kernel(int p, const double* __restrict__ partials, float* result) {
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     int64_t p2 = 1;
     while (p2 < p) p2 <<= 1;
@@ -119,6 +121,28 @@ int64_t grid_for(int64_t work_ctas, const void* fn, int threads, size_t smem, bo
 inline bool misaligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3) != 0; }
 inline int align_class(uintptr_t a) { return (a & 31) == 0 ? 8 : ((a & 15) == 0 ? 4 : 1); }
 
+#ifndef LIFT_PDL
+#define LIFT_PDL 1  // launch with programmatic stream serialization (common.cuh pdl_wait)
+#endif
+
+// Launch `k` on `s`; with LIFT_PDL the launch may overlap the previous kernel's drain
+// (every lift kernel starts with pdl_wait()).
+template <typename... KArgs, typename... Args>
+void launch(void (*k)(KArgs...), int64_t grid, int block, size_t smem, cudaStream_t s,
+            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = LIFT_PDL ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 lift_status launched() {
     return cudaGetLastError() == cudaSuccess ? LIFT_OK : LIFT_ERR_CUDA;
 }
@@ -182,7 +206,7 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
         a.rank = xa.rank;
         a.epoch = xa.epoch;
         a.error = xa.error;
-        xchg_only_kernel<<<1, 32, 0, stream>>>(a);
+        launch(xchg_only_kernel, 1, 32, 0, stream, a);
         return launched();
     }
     if (n == 0) {  // reduce over an empty array yields z = +0; no map
@@ -223,16 +247,16 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
                              : (const void*)reduce_kernel<Op, 1, B>;
     const int64_t grid = grid_for(L.nc, fn, RED_T, 0, LIFT_PERSISTENT);
-    if (lw == 8) reduce_kernel<Op, 8, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
-    else if (lw == 4) reduce_kernel<Op, 4, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
-    else reduce_kernel<Op, 1, B><<<(unsigned)grid, RED_T, 0, stream>>>(a);
+    if (lw == 8) launch(reduce_kernel<Op, 8, B>, grid, RED_T, 0, stream, a);
+    else if (lw == 4) launch(reduce_kernel<Op, 4, B>, grid, RED_T, 0, stream, a);
+    else launch(reduce_kernel<Op, 1, B>, grid, RED_T, 0, stream, a);
     return launched();
 }
 
 template <int LW, bool ALIAS>
 void scal_go(int64_t grid, int64_t nslots, int head, int tail, float alpha, const float* x,
              float* y, cudaStream_t s) {
-    scal_kernel<LW, ALIAS><<<(unsigned)grid, SCAL_T, 0, s>>>(nslots, head, tail, alpha, x, y);
+    launch(scal_kernel<LW, ALIAS>, grid, SCAL_T, 0, s, nslots, head, tail, alpha, x, y);
 }
 
 template <int LW>
@@ -265,7 +289,7 @@ lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
     const int64_t grid = grid_for(blocks, fn, NT, smem, false, true);  // CLC steals the rest
     GemvArgs b = a;
     b.nblocks = blocks;
-    gemv_kernel<NT, R, U, LW, MULTI><<<(unsigned)grid, NT, smem, s>>>(b);
+    launch(gemv_kernel<NT, R, U, LW, MULTI>, grid, NT, smem, s, b);
     return launched();
 }
 
@@ -490,7 +514,7 @@ lift_status lift_combine(int p, const double* partials, float* result, lift_stre
     if (!partials || !result) return LIFT_ERR_NULL_POINTER;
     if ((reinterpret_cast<uintptr_t>(partials) & 7) || misaligned4(result))
         return LIFT_ERR_INVALID_VALUE;
-    combine_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(p, partials, result);
+    launch(combine_kernel, 1, 32, 0, reinterpret_cast<cudaStream_t>(stream), p, partials, result);
     return launched();
 }
 
@@ -574,11 +598,11 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
     if (same) {
         const int64_t grid = grid_for((nslots + tile - 1) / tile, (const void*)blackscholes_kernel<8>,
                                       BS_T, 0, false);
-        blackscholes_kernel<8><<<(unsigned)grid, BS_T, 0, st>>>(nslots, (int)head, tail, s, call, put, p);
+        launch(blackscholes_kernel<8>, grid, BS_T, 0, st, nslots, (int)head, tail, s, call, put, p);
     } else {
         const int64_t grid = grid_for((nslots + tile - 1) / tile, (const void*)blackscholes_kernel<1>,
                                       BS_T, 0, false);
-        blackscholes_kernel<1><<<(unsigned)grid, BS_T, 0, st>>>(nslots, (int)head, tail, s, call, put, p);
+        launch(blackscholes_kernel<1>, grid, BS_T, 0, st, nslots, (int)head, tail, s, call, put, p);
     }
     return launched();
 }

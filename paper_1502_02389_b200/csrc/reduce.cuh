@@ -223,6 +223,8 @@ __device__ __forceinline__ double warp_fold_leaves(const double* leaves, int64_t
 
 // n == 0 on one rank of an all-reduce: it still has to publish (a zero) and combine.
 __global__ void xchg_only_kernel(ReduceArgs a) {
+    pdl_wait();
+    pdl_trigger();
     if (threadIdx.x < 32) xchg_combine(a, 0.0);
 }
 
@@ -404,6 +406,8 @@ __device__ __forceinline__ void trace_start(int64_t c) {
 // One CTA per chunk, hardware-scheduled (the default).
 template <class Op, int LW, int B>
 __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
     int parity = 0;
     for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x, parity ^= 1) {

@@ -34,6 +34,8 @@ __device__ __forceinline__ f8 scal_load(const float* p) {
 template <int LW, bool ALIAS>
 __global__ void __launch_bounds__(SCAL_T) scal_kernel(int64_t nslots, int head, int tail,
                                                       float alpha, const float* x, float* y) {
+    pdl_wait();
+    pdl_trigger();
     const int t = threadIdx.x;
     if (blockIdx.x == 0) {
         if (t < head) y[t] = alpha * x[t];
