@@ -4,8 +4,8 @@
 // these B200 mechanisms:
 //   asVector^8 / vect^8  -> 256-bit LDG/STG (LDG.E.ENL2.256,
 //                                                  sm_100-only; 8 fp32 per lane)
-//   toLocal                   -> shared memory, filled by the TMA
-//                                                  bulk-copy engine (cp.async.bulk)
+//   toLocal                   -> gemv's x: the SM's L1 (one copy
+//                                                  serves every resident CTA; gemv.cuh)
 //   iterate^k(split-2 reduce) in local memory    -> __shfl_xor butterfly
 //   reduce-seq                -> a per-thread register fold
 #pragma once
@@ -110,43 +110,6 @@ __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// ---- mbarrier + TMA bulk copy (cp.async.bulk -> SASS UBLKCP) -------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst_smem)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-            "selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-
 // ---- NEXT-1 peer-memory exchange primitives (reduce.cuh, gemv.cuh) -----------------
 // Exchange buffer of one rank: [2 banks x p slots of XchgSlot][2 u64 counters].
 struct XchgSlot {
@@ -183,49 +146,6 @@ __device__ __forceinline__ bool xchg_wait_flag(void* own_buf, int bank_base, int
         if (++spins > (1ull << 26)) return false;
     }
     return true;
-}
-
-// ---- Cluster Launch Control (sm_100): hardware work stealing -------------------------
-// A resident CTA cancels a not-yet-launched CTA of the same grid and takes over its
-// blockIdx (SASS UGETNEXTWORKID).  This gives persistent CTAs (per-CTA setup such as
-// gemv's x staging paid once) with the dynamic load balance of a one-CTA-per-unit grid.
-// Protocol: thread 0 issues clc_try_cancel early (before the current unit's work);
-// after the work, every thread calls clc_fetch; a __syncthreads must separate
-// clc_fetch from the next clc_try_cancel (the response buffer is reused).  After a
-// failed fetch the CTA must not issue another request.
-struct Clc {
-    uint4* resp;    // 16-byte response, shared memory
-    uint64_t* bar;  // mbarrier (count 1), shared memory
-    uint32_t phase;
-};
-
-__device__ __forceinline__ void clc_try_cancel(const Clc& c) {
-    mbar_arrive_expect_tx(c.bar, 16);
-    asm volatile(
-        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 "
-        "[%0], [%1];" ::"r"(smem_u32(c.resp)),
-        "r"(smem_u32(c.bar))
-        : "memory");
-}
-
-// Returns true and the stolen CTA's blockIdx.x in `next`, or false (no work left).
-__device__ __forceinline__ bool clc_fetch(Clc& c, int64_t& next) {
-    mbar_wait(c.bar, c.phase);
-    c.phase ^= 1u;
-    uint32_t ok, cx;
-    asm volatile(
-        "{ .reg .b128 r; .reg .pred p; ld.shared.b128 r, [%2]; "
-        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r; selp.u32 %0, 1, 0, p; "
-        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r; }"
-        : "=r"(ok), "=r"(cx)
-        : "r"(smem_u32(c.resp))
-        : "memory");
-    next = cx;
-#ifndef LIFT_CLC_NOFENCE
-    // order this generic read of the response before the next try_cancel's async write
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-    return ok != 0;
 }
 
 }  // namespace lift

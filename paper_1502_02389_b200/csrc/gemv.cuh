@@ -5,56 +5,42 @@
 //
 // A is row-major with leading dimension lda (map(..., A) maps over rows, P:815;
 // DESIGN.md reading R8).  "The dot-product from gemv might be implemented in a
-// totally different way from the stand-alone dot-product" — and it is:
+// totally different way from the stand-alone dot-product"; here it is the
+// reduction kernel's shape applied per row — m independent dots, one CTA holding
+// 256/TR rows, hardware-scheduled:
 //
-//  G1 toLocal(x): x is staged once per resident CTA (per column panel of
-//     up to GEMV_PMAX columns) by the TMA bulk-copy engine (cp.async.bulk -> UBLKCP,
-//     an mbarrier counts the bytes) through a small fp32 staging buffer, and widened
-//     to fp64 in a slot-major shared layout xs[e][q] = x[8q + e], so the per-lane
-//     reads below are conflict-free LDS.64.  x is reused by every row the CTA folds.
-//  G2 per-row dot, exact products, fp64 accumulation.  A WARP OWNS WHOLE ROWS (no
-//     cross-warp combine per row): lane l owns the 8-float vectors l, l+32, l+64, ...
-//     of a row (reorder-stride, s = 32; coalesced 256-bit LDG), 8 fp64 accumulators
-//     per row and lane fold acc_e = fma(A_ij, x_j, acc_e) in ascending vector order
-//     (A_ij * x_j is exact in fp64, so each step rounds once); lane value = pairwise
-//     fold of the 8 accumulators, then the warp butterfly xor 1..16.  A warp carries
-//     GEMV_R rows at once (each x slot read from shared memory feeds GEMV_R rows) and
-//     keeps GEMV_U k-steps of loads in flight per row.
+//  G1 toLocal(x): x is read through the SM's L1 (ld.global.nc with an
+//     evict_last hint), where every CTA resident on the SM shares one copy — x is
+//     32-64 KiB at the paper's sizes, so after the first row it is an L1
+//     hit; A streams past L1 (L1::no_allocate).
+//  G2 per-row dot, exact products, fp64 accumulation, in a canonical order that
+//     depends on n only (reading R5/R13): TR = threads per row = the largest power of two
+//     in [32, 256] with 4*TR <= ceil(n/8) (else 32); thread t' < TR owns the 8-float
+//     vectors t' + TR*k (reorder-stride, s = TR; coalesced 256-bit LDG) and folds them
+//     into 8 fp64 slot accumulators, acc_e = fma(A_ij, x_j, acc_e) in ascending k
+//     (A_ij * x_j is exact in fp64, so each step rounds once); the partial last vector
+//     (n % 8 != 0) is the last vector of its owner; thread value = pairwise fold of the
+//     8 accumulators; warp butterfly (xor 1..16); the row's TR/32 warp values pairwise.
+//     Each thread keeps GEMV_B = 4 vectors (32 KiB per CTA) of A in flight.
 //  G3 fused epilogue (rule 5f map-map fusion): y_out_i = fp32(fma(alpha, d_i,
 //     beta * y_i)) in fp64, rounded once (reading R10).  y_out may alias y.
 //
-// Scheduling: one CTA per block of (warps x GEMV_R) rows is launched; resident CTAs
-// steal the not-yet-launched blocks with Cluster Launch Control, so x is staged once
-// per resident CTA while the hardware balances rows across SMs.
+// Why one CTA per row (n >= 8192) rather than one warp per row: a whole 32 KiB row is
+// an ~11 us task for a single warp at its share of HBM bandwidth, so the last wave of
+// rows left SMs idle (the time stepped by ~9 us per extra wave, scripts/gemv_msweep.py);
+// a CTA finishes a row in ~2-3 us, and the hardware balances ~14 CTAs per resident slot.
 //
-// The order of every addition is a function of n only (not of m, the grid, the
-// row-to-warp assignment, the load width or the panel count, since panels are
-// multiples of 256 columns), so a row's bits are the same however rows are sharded.
-//
-// (A split-K variant — 8 warps per row, A rows streamed through a TMA ring by a
-// producer warp — was built and measured: 5.4-5.6 TB/s at 8192x16384 but only
-// 4.1-4.6 TB/s at 8192x8192, bounded by the per-row cross-warp combine; see
-// profiles/.  Whole rows per warp won at the bench size.)
+// The order of every addition is a function of n only (not of m, the grid, the load
+// width or alignment), so a row's bits are the same however rows are sharded.
 #pragma once
 #include "common.cuh"
 #include "canon.h"
 
 namespace lift {
 
-#ifndef LIFT_GEMV_R
-#define LIFT_GEMV_R 2  // rows per warp
-#endif
-#ifndef LIFT_GEMV_U
-#define LIFT_GEMV_U 4  // k-steps of loads in flight per row
-#endif
-constexpr int GEMV_R = LIFT_GEMV_R;
-constexpr int GEMV_U = LIFT_GEMV_U;
-constexpr int GEMV_PMAX = 16384;             // max x-panel columns staged in shared memory
-#ifndef LIFT_GEMV_XSTG
-#define LIFT_GEMV_XSTG 4096
-#endif
-constexpr int GEMV_XSTG = LIFT_GEMV_XSTG;     // fp32 staging buffer (floats) for the bulk copy
-constexpr int GEMV_SMEM_LIMIT = 227 * 1024;  // opt-in dynamic shared memory per CTA
+constexpr int GEMV_T = 256;  // threads per CTA
+constexpr int GEMV_B = 4;    // vectors per thread in flight (fixes TR's threshold too)
+constexpr int GEMV_MINB = 4;  // resident CTAs per SM: 64 registers, ~128 KiB of A in flight per SM
 
 struct GemvArgs {
     int64_t m, n, lda;
@@ -63,8 +49,7 @@ struct GemvArgs {
     const float* x;
     const float* y;
     float* y_out;
-    int P;          // panel columns (multiple of 256, <= GEMV_PMAX)
-    int xs_stride;  // doubles per slot row of xs (= P/8 + 1, padding breaks bank conflicts)
+    int64_t nblocks;  // row blocks (of 256/TR rows) of this launch
     // NEXT-1 fused all-gather of y (null y_peers: plain local y_out)
     float* const* y_peers;  // p pointers: every rank's full-length y (IPC-mapped)
     int64_t row0;           // global row of local row 0
@@ -72,123 +57,38 @@ struct GemvArgs {
     int p, rank;
     unsigned long long epoch;
     int* error;
-    int64_t nblocks;        // row blocks of this launch
 };
 
-__host__ __device__ constexpr size_t gemv_smem_bytes(int P) {
-    return 64 /*barriers*/ + (size_t)GEMV_XSTG * 4 /*fp32 stage*/ +
-           (size_t)8 * (P / 8 + 1) * 8 /*fp64 slot-major x*/;
+// log2 of the threads per row for n columns (canonical: a function of n only).
+__host__ __device__ constexpr int gemv_tr_log2(int64_t n) {
+    const int64_t nvc = (n + 7) / 8;
+    int l = 8;
+    while (l > 5 && nvc < ((int64_t)GEMV_B << l)) --l;
+    return l;
 }
 
-// Stage x[c0, c0+pc) into xs (fp64, slot-major).  Called by the whole CTA.
-template <int NT>
-__device__ __forceinline__ void gemv_stage_x(const GemvArgs& a, int64_t c0, int pc,
-                                             uint64_t* bar, float* xstage, double* xs,
-                                             uint32_t& phase) {
-    const int t = threadIdx.x;
-    for (int p0 = 0; p0 < pc; p0 += GEMV_XSTG) {
-        const int len = min(GEMV_XSTG, pc - p0);
-        const float* src = a.x + c0 + p0;
-        const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-        const int nbulk = aligned ? (len & ~3) : 0;  // elements moved by the TMA bulk copy
-        if (t == 0 && nbulk > 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive_expect_tx(bar, (uint32_t)nbulk * 4u);
-            bulk_g2s(xstage, src, (uint32_t)nbulk * 4u, bar);
-        }
-        for (int j = nbulk + t; j < len; j += NT) xstage[j] = __ldg(src + j);
-        __syncthreads();
-        if (nbulk > 0) {
-            mbar_wait(bar, phase);
-            phase ^= 1u;
-        }
-        for (int j = t; j < len; j += NT) {
-            const int jj = p0 + j;
-            xs[(jj & 7) * a.xs_stride + (jj >> 3)] = (double)xstage[j];
-        }
-        __syncthreads();  // xstage is reused by the next piece
-    }
-    // zero the padding slots of the last vector (columns pc .. round_up(pc, 8))
-    for (int jj = pc + t; jj < ((pc + 7) & ~7); jj += NT)
-        xs[(jj & 7) * a.xs_stride + (jj >> 3)] = 0.0;
-    __syncthreads();
-}
-
-// Fold panel columns [c0, c0+pc) of rows `rows[0..R)` into acc (lane-owned vectors).
-template <int R, int U, int LW>
-__device__ __forceinline__ void gemv_panel(const GemvArgs& a, const int64_t* rows, int64_t c0,
-                                           int pc, const double* xs, double (&acc)[R][8]) {
-    const int lane = threadIdx.x & 31;
-    const int kfull = pc / 256;  // k-steps where all 32 lanes hold a full vector
-    const float* rowp[R];
+// x through L1: one copy per SM serves every resident CTA (G1).
+template <int LW>
+__device__ __forceinline__ f8 ld_x(const float* p) {
+    if constexpr (LW == 8) {
+        f8 r;
+        asm("ld.global.nc.L1::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+              "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+            : "l"(p));
+        return r;
+    } else if constexpr (LW == 4) {
+        f8 r;
+        const float4 u = __ldg(reinterpret_cast<const float4*>(p));
+        const float4 w = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
+        r.v[4] = w.x; r.v[5] = w.y; r.v[6] = w.z; r.v[7] = w.w;
+        return r;
+    } else {
+        f8 r;
 #pragma unroll
-    for (int r = 0; r < R; ++r) rowp[r] = a.A + rows[r] * a.lda + c0;
-
-    int k = 0;
-    for (; k + U <= kfull; k += U) {
-        f8 av[U][R];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                av[u][r] = ld_slot<LW>(rowp[r] + 8 * (lane + 32 * (k + u)));
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int q = lane + 32 * (k + u);
-            double xv[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) xv[e] = xs[e * a.xs_stride + q];
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    acc[r][e] = __fma_rn((double)av[u][r].v[e], xv[e], acc[r][e]);
-        }
-    }
-    for (; k < kfull; ++k) {
-        const int q = lane + 32 * k;
-        f8 av[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) av[r] = ld_slot<LW>(rowp[r] + 8 * q);
-        double xv[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) xv[e] = xs[e * a.xs_stride + q];
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[r][e] = __fma_rn((double)av[r].v[e], xv[e], acc[r][e]);
-    }
-    if (kfull * 256 < pc) {  // ragged last k-step: same order, columns >= pc skipped
-        const int q = lane + 32 * kfull;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int j = 8 * q + e;
-            if (j < pc) {
-                const double xj = xs[e * a.xs_stride + q];
-#pragma unroll
-                for (int r = 0; r < R; ++r)
-                    acc[r][e] = __fma_rn((double)__ldg(rowp[r] + j), xj, acc[r][e]);
-            }
-        }
-    }
-}
-
-template <int R>
-__device__ __forceinline__ void gemv_epilogue(const GemvArgs& a, const int64_t* rows, int nvalid,
-                                              double (&acc)[R][8]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const double d = warp_pairwise(pairwise8(acc[r]));
-        if (lane == r && r < nvalid) {
-            const double w = __dmul_rn((double)a.beta, (double)a.y[rows[r]]);  // scal(b, y): exact
-            const float out = __double2float_rn(__fma_rn((double)a.alpha, d, w));
-            if (a.y_peers) {  // fused all-gather: the row lands in every rank's full y
-                for (int q = 0; q < a.p; ++q) a.y_peers[q][a.row0 + rows[r]] = out;
-            } else {
-                a.y_out[rows[r]] = out;
-            }
-        }
+        for (int e = 0; e < 8; ++e) r.v[e] = __ldg(p + e);
+        return r;
     }
 }
 
@@ -202,7 +102,7 @@ __device__ __forceinline__ void gemv_block_done(const GemvArgs& a) {
     const int bank = (int)(a.epoch & 1ull);
     unsigned last = 0;
     if (lane == 0) {
-        __threadfence_system();  // this block's row stores before its count
+        __threadfence_system();  // this block's row stores (ordered by the barrier) before its count
         unsigned long long* cnt = xchg_counter(a.xpeers[a.rank], a.p, bank);
         last = (atomicAdd(cnt, 1ull) == (unsigned long long)(a.nblocks - 1));
         if (last) {
@@ -220,67 +120,96 @@ __device__ __forceinline__ void gemv_block_done(const GemvArgs& a) {
     if (!__all_sync(0xffffffffu, ok) && lane == 0 && a.error) *a.error = 1;
 }
 
-// MULTI = false: n <= P, x staged once per CTA.  MULTI = true: n > P, x re-staged per
-// panel for every row block.
-template <int NT, int R, int U, int LW, bool MULTI>
-// minBlocks = 2 for 256 threads (two CTAs per SM) gives ptxas a 128-register budget, which
-// it spends on issuing all GEMV_U x GEMV_R 256-bit loads of a step up front (measured).
-__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) gemv_kernel(GemvArgs a) {
+// TRL = log2(threads per row) = gemv_tr_log2(n); LW = load width class of A, lda and x;
+// PEERS = the NEXT-1 fused all-gather (its code in the block loop costs the plain kernel
+// ~20% through worse load scheduling, so it is a separate instantiation).
+template <int TRL, int LW, bool PEERS>
+__global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
     pdl_wait();
     pdl_trigger();
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* clc_bar = reinterpret_cast<uint64_t*>(smem + 8);
-    uint4* clc_resp = reinterpret_cast<uint4*>(smem + 16);
-    float* xstage = reinterpret_cast<float*>(smem + 64);
-    double* xs = reinterpret_cast<double*>(smem + 64 + (size_t)GEMV_XSTG * 4);
-    const int warp = threadIdx.x >> 5;
-    uint32_t phase = 0;
-    Clc clc{clc_resp, clc_bar, 0};
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        mbar_init(clc_bar, 1);
-    }
-    __syncthreads();
-    if constexpr (!MULTI) gemv_stage_x<NT>(a, 0, (int)a.n, bar, xstage, xs, phase);
-
-    constexpr int64_t rows_per_block = (int64_t)(NT / 32) * R;
-    int64_t blk = blockIdx.x;
-    while (true) {
-#ifndef LIFT_GEMV_NOCLC
-        if (threadIdx.x == 0) clc_try_cancel(clc);  // steal the next block while we work
-#endif
-        const int64_t r0 = blk * rows_per_block + (int64_t)warp * R;
-        int64_t rows[R];
+    constexpr int TR = 1 << TRL;
+    constexpr int RP = GEMV_T / TR;  // rows per block
+    constexpr int B = GEMV_B;
+    __shared__ double wv[2][GEMV_T / 32];  // warp values, double-buffered by block parity
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int tp = t & (TR - 1);  // thread within its row
+    const int64_t nv = a.n / 8;   // full vectors per row
+    const int tailn = (int)(a.n & 7);
+    int par = 0;
+    for (int64_t blk = blockIdx.x; blk < a.nblocks; blk += gridDim.x, par ^= 1) {
+        const int64_t row = blk * RP + (t >> TRL);
+        const bool live = row < a.m;
+        const float* rp = a.A + (live ? row : a.m - 1) * a.lda;  // dead rows re-read a live one
+        double acc[8];
 #pragma unroll
-        for (int r = 0; r < R; ++r) rows[r] = min(r0 + r, a.m - 1);
-        double acc[R][8];
+        for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+        int64_t k = 0;
+        for (; (k + B) * TR <= nv; k += B) {  // full batches: every vector in range
+            f8 av[B], xv[B];
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+            for (int b = 0; b < B; ++b) {
+                const int64_t q = tp + (k + b) * TR;
+                av[b] = ld_slot<LW>(rp + 8 * q);
+                xv[b] = ld_x<LW>(a.x + 8 * q);
+            }
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[r][e] = 0.0;
-        if constexpr (!MULTI) {
-            if (r0 < a.m) gemv_panel<R, U, LW>(a, rows, 0, (int)a.n, xs, acc);
-        } else {
-            for (int64_t c0 = 0; c0 < a.n; c0 += a.P) {
-                const int pc = (int)min((int64_t)a.P, a.n - c0);
-                gemv_stage_x<NT>(a, c0, pc, bar, xstage, xs, phase);
-                if (r0 < a.m) gemv_panel<R, U, LW>(a, rows, c0, pc, xs, acc);
-                __syncthreads();  // all warps done with xs before the next panel
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    acc[e] = __fma_rn((double)av[b].v[e], (double)xv[b].v[e], acc[e]);
+        }
+        if (k * TR < nv) {  // last batch: vectors >= nv are masked to +0 x +0
+            f8 av[B], xv[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int64_t q0 = tp + (k + b) * TR;
+                const bool in = q0 < nv;
+                const int64_t q = in ? q0 : nv - 1;  // a valid address; the value is masked
+                av[b] = ld_slot<LW>(rp + 8 * q);
+                xv[b] = ld_x<LW>(a.x + 8 * q);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    av[b].v[e] = in ? av[b].v[e] : 0.f;
+                    xv[b].v[e] = in ? xv[b].v[e] : 0.f;
+                }
+            }
+            // adding +0 never changes an accumulator that started at +0 (RN: +0 + -0 = +0),
+            // so the masked slots leave the order of the real terms untouched
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    acc[e] = __fma_rn((double)av[b].v[e], (double)xv[b].v[e], acc[e]);
+        }
+        if (tailn && tp == (int)(nv & (TR - 1))) {  // the partial last vector, by its owner
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (e < tailn)
+                    acc[e] = __fma_rn((double)__ldg(rp + 8 * nv + e), (double)__ldg(a.x + 8 * nv + e),
+                                      acc[e]);
+        }
+        const double v = warp_pairwise(pairwise8(acc));
+        if (lane == 0) wv[par][warp] = v;
+        __syncthreads();
+        if (tp == 0 && live) {
+            const double* w = wv[par] + (t >> 5);
+            double d;
+            if constexpr (TRL == 8) d = pairwise8(w);
+            else if constexpr (TRL == 7) d = __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3]));
+            else if constexpr (TRL == 6) d = __dadd_rn(w[0], w[1]);
+            else d = w[0];
+            const double yb = __dmul_rn((double)a.beta, (double)a.y[row]);  // scal(b, y): exact
+            const float out = __double2float_rn(__fma_rn((double)a.alpha, d, yb));
+            if constexpr (PEERS) {  // fused all-gather: the row lands in every rank's full y
+                for (int q = 0; q < a.p; ++q) a.y_peers[q][a.row0 + row] = out;
+            } else {
+                a.y_out[row] = out;
             }
         }
-        if (r0 < a.m) gemv_epilogue<R>(a, rows, (int)min((int64_t)R, a.m - r0), acc);
-        int64_t next;
-#ifndef LIFT_GEMV_NOCLC
-        const bool more = clc_fetch(clc, next);
-#else
-        const bool more = false;
-        next = 0;
-#endif
-        __syncthreads();  // everyone has read the response before it is reused
-        if (a.y_peers && warp == 0) gemv_block_done(a);  // after the barrier: rows stored
-        if (!more) break;
-        blk = next;
+        if constexpr (PEERS) {
+            __syncthreads();  // every row store of this block precedes its count
+            if (warp == 0) gemv_block_done(a);
+        }
     }
 }
 

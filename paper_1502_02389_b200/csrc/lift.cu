@@ -92,7 +92,7 @@ int occupancy(const void* fn, int threads, size_t smem) {
     // The attribute is a per-function maximum: set it to the largest opt-in size once,
     // so launches with any smaller dynamic smem (other n) stay valid.
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMV_SMEM_LIMIT);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess ||
         b < 1)
@@ -264,64 +264,38 @@ const void* scal_fn(bool alias) {
     return alias ? (const void*)scal_kernel<LW, true> : (const void*)scal_kernel<LW, false>;
 }
 
-#ifndef LIFT_GEMV_SMALL
-#define LIFT_GEMV_SMALL 1  // short-m path (fewer rows per block); 0 disables
-#endif
-#ifndef LIFT_GEMV_SMALL_ROWS_PER_SM
-#define LIFT_GEMV_SMALL_ROWS_PER_SM 24  // use it when m < this x SMs (1.5 default blocks per SM)
-#endif
-#ifndef LIFT_GEMV_SNT
-#define LIFT_GEMV_SNT 256
-#endif
-#ifndef LIFT_GEMV_SR
-#define LIFT_GEMV_SR 1
-#endif
-#ifndef LIFT_GEMV_SU
-#define LIFT_GEMV_SU 8
-#endif
-
-template <int NT, int R, int U, int LW, bool MULTI>
-lift_status gemv_go(const GemvArgs& a, cudaStream_t s) {
-    const size_t smem = gemv_smem_bytes(a.P);
-    const void* fn = (const void*)gemv_kernel<NT, R, U, LW, MULTI>;
-    const int64_t rows_per_cta = (int64_t)(NT / 32) * R;
-    const int64_t blocks = (a.m + rows_per_cta - 1) / rows_per_cta;
-    const int64_t grid = grid_for(blocks, fn, NT, smem, false, true);  // CLC steals the rest
-    GemvArgs b = a;
-    b.nblocks = blocks;
-    launch(gemv_kernel<NT, R, U, LW, MULTI>, grid, NT, smem, s, b);
+template <int TRL, int LW, bool PEERS>
+lift_status gemv_go(GemvArgs a, cudaStream_t s) {
+    constexpr int64_t rp = GEMV_T >> TRL;  // rows per block
+    a.nblocks = (a.m + rp - 1) / rp;
+    const void* fn = (const void*)gemv_kernel<TRL, LW, PEERS>;
+    const int64_t grid = grid_for(a.nblocks, fn, GEMV_T, 0, LIFT_PERSISTENT);
+    launch(gemv_kernel<TRL, LW, PEERS>, grid, GEMV_T, 0, s, a);
     return launched();
 }
 
-template <int NT, int R, int U>
-lift_status gemv_pick(const GemvArgs& a, int lw, bool multi, cudaStream_t s) {
-    if (multi)
-        return lw == 8 ? gemv_go<NT, R, U, 8, true>(a, s) : lw == 4 ? gemv_go<NT, R, U, 4, true>(a, s)
-                                                                   : gemv_go<NT, R, U, 1, true>(a, s);
-    return lw == 8 ? gemv_go<NT, R, U, 8, false>(a, s) : lw == 4 ? gemv_go<NT, R, U, 4, false>(a, s)
-                                                                : gemv_go<NT, R, U, 1, false>(a, s);
+template <int TRL, bool PEERS>
+lift_status gemv_lw(const GemvArgs& a, int lw, cudaStream_t s) {
+    return lw == 8 ? gemv_go<TRL, 8, PEERS>(a, s)
+         : lw == 4 ? gemv_go<TRL, 4, PEERS>(a, s) : gemv_go<TRL, 1, PEERS>(a, s);
 }
 
-lift_status gemv_launch(GemvArgs a, cudaStream_t s) {
-    const bool multi = a.n > GEMV_PMAX;
-    a.P = multi ? GEMV_PMAX : (int)(((a.n > 0 ? a.n : 1) + 255) / 256 * 256);
-    a.xs_stride = a.P / 8 + 1;
-    const uintptr_t aa = reinterpret_cast<uintptr_t>(a.A);
-    const int lw = ((aa & 31) == 0 && a.lda % 8 == 0) ? 8 : ((aa & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
-    const bool two = 2 * gemv_smem_bytes(a.P) <= (size_t)GEMV_SMEM_LIMIT;
-#if LIFT_GEMV_SMALL
-    // Short m: the default 16-row blocks would leave SMs without a CTA (m = 1024 -> 64
-    // blocks on 148 SMs).  One row per warp (8-row blocks) with 8 k-steps of loads in
-    // flight instead (measured, scripts/ab_gemv.py: 1024x8192 14.3 -> 10.9 us, 2048x8192
-    // 16.4 -> 14.7 us); every (NT, R, U) gives the same bits (each row's order is fixed
-    // by the lane/slot map).
-    if (two && a.m < (int64_t)LIFT_GEMV_SMALL_ROWS_PER_SM * sm_count(current_device()))
-        return gemv_pick<LIFT_GEMV_SNT, LIFT_GEMV_SR, LIFT_GEMV_SU>(a, lw, multi, s);
-#endif
-    // Two 256-thread CTAs per SM while x fits twice in shared memory; otherwise one
-    // 512-thread CTA, so an SM always runs 16 warps.
-    if (two) return gemv_pick<256, GEMV_R, GEMV_U>(a, lw, multi, s);
-    return gemv_pick<512, GEMV_R, GEMV_U>(a, lw, multi, s);
+template <bool PEERS>
+lift_status gemv_trl(const GemvArgs& a, int lw, cudaStream_t s) {
+    switch (gemv_tr_log2(a.n)) {  // threads per row: part of the canonical order (n only)
+        case 8: return gemv_lw<8, PEERS>(a, lw, s);
+        case 7: return gemv_lw<7, PEERS>(a, lw, s);
+        case 6: return gemv_lw<6, PEERS>(a, lw, s);
+        default: return gemv_lw<5, PEERS>(a, lw, s);
+    }
+}
+
+lift_status gemv_launch(const GemvArgs& a, cudaStream_t s) {
+    // the widest load class that A's rows (base + lda) and x all allow; the order of the
+    // arithmetic does not depend on it (gemv.cuh)
+    const uintptr_t al = reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.x);
+    const int lw = ((al & 31) == 0 && a.lda % 8 == 0) ? 8 : ((al & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
+    return a.y_peers ? gemv_trl<true>(a, lw, s) : gemv_trl<false>(a, lw, s);
 }
 
 }  // namespace

@@ -1,13 +1,11 @@
-"""gemv's Cluster-Launch-Control work stealing under repetition.
+"""gemv under repetition: many launches into NaN-filled outputs at shapes with thousands
+of row blocks per launch must write every row, with the same bits every time.
 
-Row blocks are launched one CTA each; a resident CTA cancels a pending CTA
-(`clusterlaunchcontrol.try_cancel`) and runs its block.  Every CTA reads the 16-byte
-response with generic loads and the next try_cancel rewrites it through the async
-proxy; without a `fence.proxy.async.shared::cta` between the two, a warp could act on
-the wrong response and skip its rows (measured: 25 of 400 launches at 8192 x 8192 left
-one warp's two rows unwritten or half-summed).  This test repeats launches into
-NaN-filled outputs at shapes with hundreds of steals per launch and requires every
-launch to write every row with the same bits."""
+(History: an earlier gemv design stole row blocks with Cluster Launch Control; without a
+proxy fence between reading the CLC response and the next try_cancel, 25 of 400
+launches at 8192 x 8192 left one warp's rows unwritten.  Tolerance tests on recycled
+output buffers had passed; this test is what caught it, and it stays for any
+scheduling change.)"""
 import numpy as np
 import pytest
 import torch

@@ -414,3 +414,58 @@ def test_full_dot_2p31(lift):
         s.dot(xb, yb)
     o = s.value()
     assert abs(g - o) <= 1e-5 * o
+
+
+# ------------------------------ canonical order: bits depend on n only (rounded sums)
+def rough(n, seed, lo_exp=-20, hi_exp=20):
+    """Full-mantissa values over a wide exponent range: fp64 sums of their products
+    round, so any change of summation order shows up in the bits (the 2^-24-grid
+    generator inputs sum exactly and cannot detect it)."""
+    r = np.random.default_rng(seed)
+    v = r.standard_normal(n) * np.exp2(r.integers(lo_exp, hi_exp, n))
+    return v.astype(np.float32)
+
+
+@pytest.mark.parametrize("m,n", [(300, 8192), (70, 3001), (130, 16384 + 9), (9, 5)])
+def test_gemv_order_depends_on_n_only(lift, m, n):
+    A = rough(m * n, 1).reshape(m, n)
+    x, y = rough(n, 2), rough(m, 3)
+    ref = bits(lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5))
+    check_gemv(lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5).cpu().numpy(), A, x, y, 1.5, 0.5)
+    # load width / alignment: A offset by 1 and 4 floats, padded lda, x offset
+    for off, pad in [(1, 0), (4, 0), (0, 3), (0, 8)]:
+        buf = torch.zeros(m * (n + pad) + off + 8, dtype=torch.float32, device=DEV)
+        Av = buf[off:off + m * (n + pad)].view(m, n + pad)[:, :n]
+        Av.copy_(dev(A))
+        xb = torch.zeros(n + 8, dtype=torch.float32, device=DEV)
+        xv = xb[off:off + n]
+        xv.copy_(dev(x))
+        assert np.array_equal(bits(lift.gemv(Av, xv, dev(y), 1.5, 0.5)), ref), (off, pad)
+    # row subsets (sharding) and a capped grid
+    for a, b in [(0, 1), (m // 3, m // 3 + 7), (m - 1, m)]:
+        assert np.array_equal(bits(lift.gemv(dev(A[a:b]), dev(x), dev(y[a:b]), 1.5, 0.5)), ref[a:b])
+    try:
+        lift.set_grid_limit(2)
+        assert np.array_equal(bits(lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5)), ref)
+    finally:
+        lift.set_grid_limit(0)
+
+
+@pytest.mark.parametrize("n", [3001, (1 << 21) + 7])
+def test_reduce_order_depends_on_n_only(lift, n):
+    x, y = rough(n, 4), rough(n, 5)
+    ra, rd = bits(lift.asum(dev(x))), bits(lift.dot(dev(x), dev(y)))
+    for off in (1, 4):
+        xb = torch.zeros(n + 8, dtype=torch.float32, device=DEV)
+        yb = torch.zeros(n + 8, dtype=torch.float32, device=DEV)
+        xv, yv = xb[off:off + n], yb[off:off + n]
+        xv.copy_(dev(x))
+        yv.copy_(dev(y))
+        assert np.array_equal(bits(lift.asum(xv)), ra)
+        assert np.array_equal(bits(lift.dot(xv, yv)), rd)
+    try:
+        lift.set_grid_limit(3)
+        assert np.array_equal(bits(lift.asum(dev(x))), ra)
+        assert np.array_equal(bits(lift.dot(dev(x), dev(y))), rd)
+    finally:
+        lift.set_grid_limit(0)
