@@ -25,6 +25,10 @@ KEYS = [
     ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
     ("smsp__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_pipe_%"),
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lsu_pipe_%"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_pipe_%"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "alu_pipe_%"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "fma_pipe_%"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64_pipe_sm_%"),
     ("smsp__average_warp_latency_issue_stalled_long_scoreboard", "stall_long_sb"),
     ("smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct", "stall_long_sb_%"),
     ("smsp__warp_issue_stalled_barrier_per_warp_active.pct", "stall_barrier_%"),
