@@ -188,9 +188,11 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
  *   call[i] = s_i N(d1) - K e^{-rT} N(d2),  put[i] = K e^{-rT} N(-d2) - s_i N(-d1),
  *   d1 = (ln(s_i/K) + (r + v^2/2) T) / (v sqrt T),  d2 = d1 - v sqrt T,  N = normal CDF
  *   (closed form; the paper does not print the helpers, P:825 — DESIGN.md reading R22).
- *   s: n floats in (prices > 0); call, put: n floats out (SoA).  fp32 arithmetic with
- *   IEEE-accurate logf/expf/erfcf (no fast math).  K, v, T must be > 0 and finite, r
- *   finite, else LIFT_ERR_INVALID_VALUE.  n == 0 launches nothing. */
+ *   s: n floats in (prices > 0); call, put: n floats out (SoA).  fp32 arithmetic: N(-|d|)
+ *   by the Abramowitz-Stegun 26.2.17 polynomial (|error| < 7.5e-8), log2/exp2/rcp by the
+ *   hardware approximations (reading R22); per-option error <= 1e-6 (s + K)
+ *   against the fp64 oracle.  K, v, T must be > 0 and finite, r finite, else
+ *   LIFT_ERR_INVALID_VALUE.  n == 0 launches nothing. */
 lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,
                               float* call, float* put, lift_stream_t stream);
 

@@ -21,7 +21,9 @@ constexpr long long RED_C = (long long)RED_T * RED_V * RED_K;  // elements per c
 constexpr int RED_G = LIFT_RED_G;                 // chunks per group (level-1 fold)
 static_assert(RED_G <= RED_T, "group fold uses one leaf per thread");
 
-// gemv: the row order is defined in gemv.cuh (chunks of min(8192, round_up(n,1024))
-// columns, 8 warp segments, 4-float lane vectors, 4 fp64 lane accumulators).
+// gemv: the row order is defined in gemv.cuh: TR = gemv_tr_log2(n) threads per row
+// (256 for n >= 8192, halving to 32), thread t' owns the 8-float vectors t' + TR*k,
+// 8 fp64 slot accumulators in ascending k, pairwise8, warp butterfly, the row's TR/32
+// warp values pairwise.
 
 }  // namespace lift

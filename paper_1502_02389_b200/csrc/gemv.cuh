@@ -38,9 +38,16 @@
 
 namespace lift {
 
+#ifndef LIFT_GEMV_B
+#define LIFT_GEMV_B 4     // vectors per thread in flight (launch shape only, not the order)
+#endif
+#ifndef LIFT_GEMV_MINB
+#define LIFT_GEMV_MINB 4  // resident CTAs per SM: 64 registers, ~128 KiB of A in flight per SM
+#endif
 constexpr int GEMV_T = 256;  // threads per CTA
-constexpr int GEMV_B = 4;    // vectors per thread in flight (fixes TR's threshold too)
-constexpr int GEMV_MINB = 4;  // resident CTAs per SM: 64 registers, ~128 KiB of A in flight per SM
+constexpr int GEMV_B = LIFT_GEMV_B;
+constexpr int GEMV_MINB = LIFT_GEMV_MINB;
+constexpr int GEMV_TR_V = 4;  // canonical: TR is the largest power of two with 4*TR <= ceil(n/8)
 
 struct GemvArgs {
     int64_t m, n, lda;
@@ -63,7 +70,7 @@ struct GemvArgs {
 __host__ __device__ constexpr int gemv_tr_log2(int64_t n) {
     const int64_t nvc = (n + 7) / 8;
     int l = 8;
-    while (l > 5 && nvc < ((int64_t)GEMV_B << l)) --l;
+    while (l > 5 && nvc < ((int64_t)GEMV_TR_V << l)) --l;
     return l;
 }
 

@@ -29,10 +29,10 @@ SPACE = {
               ("k16", "-DLIFT_RED_K=16 -DLIFT_RED_G=64")],
     "asum_acc": [("asum_f32", "-DLIFT_ASUM_ACC=float"), ("asum_f64", "-DLIFT_ASUM_ACC=double")],
     "dot_acc": [("dot_f64", "-DLIFT_DOT_ACC=double"), ("dot_f32", "-DLIFT_DOT_ACC=float")],
-    "gemv_ru": [("g_r1u8", "-DLIFT_GEMV_R=1 -DLIFT_GEMV_U=8"),
-                ("g_r2u4", "-DLIFT_GEMV_R=2 -DLIFT_GEMV_U=4"),
-                ("g_r2u2", "-DLIFT_GEMV_R=2 -DLIFT_GEMV_U=2"),
-                ("g_r4u2", "-DLIFT_GEMV_R=4 -DLIFT_GEMV_U=2")],
+    "gemv_b": [("g_b4m4", "-DLIFT_GEMV_B=4 -DLIFT_GEMV_MINB=4"),
+               ("g_b2m6", "-DLIFT_GEMV_B=2 -DLIFT_GEMV_MINB=6"),
+               ("g_b8m2", "-DLIFT_GEMV_B=8 -DLIFT_GEMV_MINB=2"),
+               ("g_b4m3", "-DLIFT_GEMV_B=4 -DLIFT_GEMV_MINB=3")],
     "grid": [("nonpersistent", "-DLIFT_PERSISTENT=0"), ("persistent", "-DLIFT_PERSISTENT=1")],
 }
 
