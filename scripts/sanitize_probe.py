@@ -34,7 +34,8 @@ lift.combine(torch.rand(5, dtype=torch.float64, device=dev))
 x = rnd(1000)
 x[7] = float("inf")
 lift.asum(x)  # fp64 refold path
-for m, n, pad in [(3, 5, 0), (40, 1000, 3), (40, 8192, 0), (17, 9000, 4), (5, 20000, 0)]:
+for m, n, pad in [(3, 5, 0), (40, 1000, 3), (30, 3001, 1), (9, 4100, 0), (40, 8192, 0), (6, 8195, 2),
+                 (17, 9000, 4), (5, 20000, 0)]:
     A = torch.rand(m, n + pad, generator=g).to(dev)[:, :n]
     lift.gemv(A, rnd(n), rnd(m), 1.5, 0.5)
 torch.cuda.synchronize()
