@@ -253,10 +253,14 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     return launched();
 }
 
+#ifndef LIFT_SCAL_SMEM
+#define LIFT_SCAL_SMEM 0  // (A/B knob) dynamic smem reserved per CTA: caps resident CTAs per SM
+#endif
+
 template <int LW, bool ALIAS>
 void scal_go(int64_t grid, int64_t nslots, int head, int tail, float alpha, const float* x,
              float* y, cudaStream_t s) {
-    launch(scal_kernel<LW, ALIAS>, grid, SCAL_T, 0, s, nslots, head, tail, alpha, x, y);
+    launch(scal_kernel<LW, ALIAS>, grid, SCAL_T, LIFT_SCAL_SMEM, s, nslots, head, tail, alpha, x, y);
 }
 
 template <int LW>
@@ -346,7 +350,7 @@ lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_str
     const bool alias = (x == y);
     const void* fn = lw == 8 ? scal_fn<8>(alias) : lw == 4 ? scal_fn<4>(alias) : scal_fn<1>(alias);
     const int64_t tile = (int64_t)SCAL_T * SCAL_U;
-    const int64_t grid = grid_for((nslots + tile - 1) / tile, fn, SCAL_T, 0, LIFT_PERSISTENT);
+    const int64_t grid = grid_for((nslots + tile - 1) / tile, fn, SCAL_T, LIFT_SCAL_SMEM, LIFT_PERSISTENT);
     if (lw == 8) alias ? scal_go<8, true>(grid, nslots, (int)head, tail, alpha, x, y, s)
                        : scal_go<8, false>(grid, nslots, (int)head, tail, alpha, x, y, s);
     else if (lw == 4) alias ? scal_go<4, true>(grid, nslots, (int)head, tail, alpha, x, y, s)

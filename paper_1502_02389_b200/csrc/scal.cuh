@@ -15,8 +15,19 @@
 
 namespace lift {
 
-constexpr int SCAL_T = 256;  // threads per CTA
-constexpr int SCAL_U = 4;    // 8-float slots per thread per tile (4 x 32 B in flight)
+// Tile = 1024 threads x 1 slot (32 KiB in, 32 KiB out), two CTAs per SM: ~64 KiB of
+// loads in flight per SM.  Measured (scripts/ab.py, 2^28): 256 x 4 (8 CTAs, 256 KiB in
+// flight) 313.9 us, 256 x 1 308.9, 512 x 1 307.7, 1024 x 1 303.9 (7.07 TB/s); capping
+// resident CTAs below full thread occupancy costs more (1024 x 1 at one CTA/SM: 447 us).
+// A read+write stream runs best with fewer bytes queued per SM.
+#ifndef LIFT_SCAL_T
+#define LIFT_SCAL_T 1024
+#endif
+#ifndef LIFT_SCAL_U
+#define LIFT_SCAL_U 1
+#endif
+constexpr int SCAL_T = LIFT_SCAL_T;  // threads per CTA
+constexpr int SCAL_U = LIFT_SCAL_U;  // 8-float slots per thread per tile
 
 template <int LW, bool ALIAS>
 __device__ __forceinline__ f8 scal_load(const float* p) {
