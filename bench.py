@@ -36,7 +36,7 @@ ALPHA_SCAL = 3.0
 ALPHA, BETA = 1.5, 0.5
 NOMINAL_HBM = 8000.0  # GB/s, BASELINE.json's denominator (nominal)
 
-OPS = ("scal", "asum", "dot", "gemv")
+OPS = tuple(os.environ.get("LIFT_STEP_ORDER", "scal,asum,dot,gemv").split(","))
 
 
 def op_bytes(world: int = 1) -> dict:
@@ -312,29 +312,37 @@ def run_lift(args):
                                   out_full=out_full, out_slice=out_slice)
     torch.cuda.synchronize()
 
-    def step(ev=None):
-        """One pass of the hot path; ev = per-op (start, end) event pairs or None."""
-        def rec(i):
-            if ev is not None:
-                ev[i].record(stream)
-        rec(0)
+    def op_scal():
         lift.scal(ALPHA_SCAL, x_v, out=y_v)
-        rec(1)
+
+    def op_asum():
         if world == 1:
             lift.asum(x_v, out=r_asum, ws=ws_a)
         else:
             x_asum(x_v, r_asum, ws_a)
-        rec(2)
+
+    def op_dot():
         if world == 1:
             lift.dot(x_d, y_d, out=r_dot, ws=ws_d)
         else:
             x_dot(x_d, y_d, r_dot, ws_d)
-        rec(3)
+
+    def op_gemv():
         if world == 1:
             lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out)
         else:
             x_gemv(A, g_x, g_y, g_full, g_out)
-        rec(4)
+
+    op_fn = {"scal": op_scal, "asum": op_asum, "dot": op_dot, "gemv": op_gemv}
+
+    def step(ev=None):
+        """One pass of the hot path (in OPS order); ev = per-op event boundaries or None."""
+        for i, op in enumerate(OPS):
+            if ev is not None:
+                ev[i].record(stream)
+            op_fn[op]()
+        if ev is not None:
+            ev[len(OPS)].record(stream)
 
     def barrier():
         if world > 1:
