@@ -15,12 +15,13 @@
 //     hit; A streams past L1 (L1::no_allocate).
 //  G2 per-row dot, exact products, fp64 accumulation, in a canonical order that
 //     depends on n only (reading R5/R13): TR = threads per row = the largest power of two
-//     in [32, 256] with 4*TR <= ceil(n/8) (else 32); thread t' < TR owns the 8-float
+//     in [1, 256] with 4*TR <= ceil(n/8) (else 1); thread t' < TR owns the 8-float
 //     vectors t' + TR*k (reorder-stride, s = TR; coalesced 256-bit LDG) and folds them
 //     into 8 fp64 slot accumulators, acc_e = fma(A_ij, x_j, acc_e) in ascending k
 //     (A_ij * x_j is exact in fp64, so each step rounds once); the partial last vector
 //     (n % 8 != 0) is the last vector of its owner; thread value = pairwise fold of the
-//     8 accumulators; warp butterfly (xor 1..16); the row's TR/32 warp values pairwise.
+//     8 accumulators; butterfly over the row's lanes (xor 1..min(TR,32)/2); for TR > 32
+//     the row's TR/32 warp values pairwise.
 //     Each thread keeps GEMV_B = 4 vectors (32 KiB per CTA) of A in flight.
 //  G3 fused epilogue (rule 5f map-map fusion): y_out_i = fp32(fma(alpha, d_i,
 //     beta * y_i)) in fp64, rounded once (reading R10).  y_out may alias y.
@@ -70,7 +71,7 @@ struct GemvArgs {
 __host__ __device__ constexpr int gemv_tr_log2(int64_t n) {
     const int64_t nvc = (n + 7) / 8;
     int l = 8;
-    while (l > 5 && nvc < ((int64_t)GEMV_TR_V << l)) --l;
+    while (l > 0 && nvc < ((int64_t)GEMV_TR_V << l)) --l;
     return l;
 }
 
@@ -195,16 +196,24 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
                     acc[e] = __fma_rn((double)__ldg(rp + 8 * nv + e), (double)__ldg(a.x + 8 * nv + e),
                                       acc[e]);
         }
-        const double v = warp_pairwise(pairwise8(acc));
-        if (lane == 0) wv[par][warp] = v;
-        __syncthreads();
-        if (tp == 0 && live) {
+        double d;
+        if constexpr (TR < 32) {
+            // rows narrower than a warp: butterfly over the row's TR lanes only (xor stays
+            // inside the aligned lane group), no shared memory, no barrier
+            d = pairwise8(acc);
+#pragma unroll
+            for (int o = 1; o < TR; o <<= 1) d = __dadd_rn(d, __shfl_xor_sync(0xffffffffu, d, o));
+        } else {
+            const double v = warp_pairwise(pairwise8(acc));
+            if (lane == 0) wv[par][warp] = v;
+            __syncthreads();
             const double* w = wv[par] + (t >> 5);
-            double d;
             if constexpr (TRL == 8) d = pairwise8(w);
             else if constexpr (TRL == 7) d = __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3]));
             else if constexpr (TRL == 6) d = __dadd_rn(w[0], w[1]);
             else d = w[0];
+        }
+        if (tp == 0 && live) {
             const double yb = __dmul_rn((double)a.beta, (double)a.y[row]);  // scal(b, y): exact
             const float out = __double2float_rn(__fma_rn((double)a.alpha, d, yb));
             if constexpr (PEERS) {  // fused all-gather: the row lands in every rank's full y

@@ -290,7 +290,12 @@ lift_status gemv_trl(const GemvArgs& a, int lw, cudaStream_t s) {
         case 8: return gemv_lw<8, PEERS>(a, lw, s);
         case 7: return gemv_lw<7, PEERS>(a, lw, s);
         case 6: return gemv_lw<6, PEERS>(a, lw, s);
-        default: return gemv_lw<5, PEERS>(a, lw, s);
+        case 5: return gemv_lw<5, PEERS>(a, lw, s);
+        case 4: return gemv_lw<4, PEERS>(a, lw, s);
+        case 3: return gemv_lw<3, PEERS>(a, lw, s);
+        case 2: return gemv_lw<2, PEERS>(a, lw, s);
+        case 1: return gemv_lw<1, PEERS>(a, lw, s);
+        default: return gemv_lw<0, PEERS>(a, lw, s);
     }
 }
 
