@@ -184,6 +184,23 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
                       const float* x, float beta, const float* y, float* y_out,
                       lift_stream_t stream);
 
+/* gemv with a workspace (same result bits as lift_gemv for every input).
+ *   Rows of n >= 65536 columns are summed in the stand-alone dot's canonical order
+ *   (y_out[i] uses exactly lift_dot_partial(A_i, x) in fp64).  When such rows are too few
+ *   to occupy the GPU with one CTA each (m < 4 x SMs), ws lets the call spread each row's
+ *   8192-column chunks over many CTAs with a per-row single-pass last-block-done.
+ *   ws: device buffer of ws_bytes >= lift_gemv_workspace_bytes(m, n), 16-byte aligned,
+ *   zero-filled ONCE by the caller (the kernels leave their tickets at zero); one
+ *   buffer per stream, reusable for any (m, n) it fits.  ws may be NULL or smaller: the
+ *   call then uses one CTA per row (same bits, fewer CTAs).  Other arguments and errors
+ *   as lift_gemv. */
+lift_status lift_gemv_ws(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
+                         const float* x, float beta, const float* y, float* y_out, void* ws,
+                         size_t ws_bytes, lift_stream_t stream);
+/* Workspace bytes for lift_gemv_ws's split path at (m, n); 0 when rows are shorter than
+ *   65536 columns (no split path). */
+size_t lift_gemv_workspace_bytes(int64_t m, int64_t n);
+
 /* NEXT-3 — BlackScholes (Fig. 9): map(BSComputation, s) over n stock prices.
  *   call[i] = s_i N(d1) - K e^{-rT} N(d2),  put[i] = K e^{-rT} N(-d2) - s_i N(-d1),
  *   d1 = (ln(s_i/K) + (r + v^2/2) T) / (v sqrt T),  d2 = d1 - v sqrt T,  N = normal CDF

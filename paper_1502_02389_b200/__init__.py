@@ -192,10 +192,11 @@ def combine(partials: torch.Tensor, out: torch.Tensor | None = None) -> torch.Te
 
 
 def gemv(A: torch.Tensor, x: torch.Tensor, y: torch.Tensor, alpha: float, beta: float,
-         out: torch.Tensor | None = None) -> torch.Tensor:
-    """y_out = alpha * A @ x + beta * y (lift_gemv), A row-major (stride(1) == 1).
+         out: torch.Tensor | None = None, split: bool = True) -> torch.Tensor:
+    """y_out = alpha * A @ x + beta * y (lift_gemv_ws), A row-major (stride(1) == 1).
 
-    ``out`` may be ``y`` (in place)."""
+    ``out`` may be ``y`` (in place).  ``split=False`` withholds the workspace, forcing one
+    CTA per row for long rows (same bits; for tests)."""
     if not (isinstance(A, torch.Tensor) and A.is_cuda and A.dtype == torch.float32
             and A.dim() == 2):
         raise ValueError("A must be a 2-D float32 CUDA tensor")
@@ -208,9 +209,29 @@ def gemv(A: torch.Tensor, x: torch.Tensor, y: torch.Tensor, alpha: float, beta: 
         raise ValueError(f"dimension-mismatch: A is {m}x{n}, x has {x.numel()}, "
                          f"y has {y.numel()}")
     yo = _out(out, m, torch.float32, A.device)
-    check(lib.lift_gemv(m, n, float(alpha), A.data_ptr(), lda, x.data_ptr(), float(beta),
-                        y.data_ptr(), yo.data_ptr(), _stream_handle(A.device)))
+    need = int(lib.lift_gemv_workspace_bytes(m, n)) if split else 0
+    wp, wb = (0, 0)
+    if need:  # rows >= 65536 columns: the split path needs a workspace (lift_gemv_ws)
+        w = _gemv_workspace(need, A.device)
+        wp, wb = w.data_ptr(), w.numel()
+    check(lib.lift_gemv_ws(m, n, float(alpha), A.data_ptr(), lda, x.data_ptr(), float(beta),
+                           y.data_ptr(), yo.data_ptr(), wp or None, wb,
+                           _stream_handle(A.device)))
     return yo
+
+
+_gemv_ws_cache: dict = {}
+
+
+def _gemv_workspace(need: int, device: torch.device) -> torch.Tensor:
+    """Zero-filled gemv split-path workspace per (device, stream), grown on demand."""
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    with _ws_lock:
+        w = _gemv_ws_cache.get(key)
+        if w is None or w.numel() < need:
+            w = torch.zeros(need, dtype=torch.uint8, device=device)
+            _gemv_ws_cache[key] = w
+        return w
 
 
 def blackscholes(s: torch.Tensor, K: float, r: float, v: float, T: float,

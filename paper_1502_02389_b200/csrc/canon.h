@@ -21,7 +21,8 @@ constexpr long long RED_C = (long long)RED_T * RED_V * RED_K;  // elements per c
 constexpr int RED_G = LIFT_RED_G;                 // chunks per group (level-1 fold)
 static_assert(RED_G <= RED_T, "group fold uses one leaf per thread");
 
-// gemv: the row order is defined in gemv.cuh: TR = gemv_tr_log2(n) threads per row
+// gemv: rows of n >= GEMV_LONG_N = 65536 use exactly the dot order above (gemv_long.cuh);
+// shorter rows the order defined in gemv.cuh: TR = gemv_tr_log2(n) threads per row
 // (256 for n >= 8192, halving down to 1 for n <= 24), thread t' owns the 8-float
 // vectors t' + TR*k, 8 fp64 slot accumulators in ascending k, pairwise8, butterfly over
 // the row's lanes, the row's TR/32 warp values pairwise (TR > 32).

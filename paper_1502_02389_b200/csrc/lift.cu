@@ -15,6 +15,7 @@
 #include "blackscholes.cuh"
 #include "gemv.cuh"
 #include "reduce.cuh"
+#include "gemv_long.cuh"
 #include "scal.cuh"
 
 #ifndef LIFT_ASUM_B
@@ -299,11 +300,63 @@ lift_status gemv_trl(const GemvArgs& a, int lw, cudaStream_t s) {
     }
 }
 
-lift_status gemv_launch(const GemvArgs& a, cudaStream_t s) {
+// Split-path workspace bytes for (m, n): partials + a ticket region of a third of W.
+size_t gemv_ws_bytes_for(int64_t m, int64_t n) {
+    if (n < GEMV_LONG_N || m <= 0) return 0;
+    const int64_t nc = (n + RED_C - 1) / RED_C, ng = (nc + RED_G - 1) / RED_G;
+    const size_t part = 8 * (size_t)m * (size_t)(nc + ng);
+    const size_t tick = 4 * (size_t)m * (size_t)(ng + 1);
+    size_t w = (part + part / 2 + 64 + 15) & ~(size_t)15;
+    while (w - gemv_ws_ticket_region(w) < part || gemv_ws_ticket_region(w) < tick) w += 16;
+    return w;
+}
+
+template <int LW>
+lift_status gemv_split_go(const GemvArgs& a, void* ws, size_t ws_bytes, cudaStream_t s) {
+    GemvSplitArgs sa{};
+    sa.g = a;
+    sa.nc = (a.n + RED_C - 1) / RED_C;
+    sa.ng = (sa.nc + RED_G - 1) / RED_G;
+    const size_t wf = ws_bytes & ~(size_t)15;
+    sa.chunk_part = static_cast<double*>(ws);
+    sa.group_part = sa.chunk_part + a.m * sa.nc;
+    sa.tick = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + wf - gemv_ws_ticket_region(wf));
+    const int64_t grid = grid_for(a.m * sa.nc, (const void*)gemv_split_kernel<LW>, RED_T, 0,
+                                  LIFT_PERSISTENT);
+    launch(gemv_split_kernel<LW>, grid, RED_T, 0, s, sa);
+    return launched();
+}
+
+template <int LW, bool PEERS>
+lift_status gemv_long_go(GemvArgs a, cudaStream_t s) {
+    a.nblocks = a.m;
+    const int64_t grid = grid_for(a.m, (const void*)gemv_long_kernel<LW, PEERS>, RED_T, 0,
+                                  LIFT_PERSISTENT);
+    launch(gemv_long_kernel<LW, PEERS>, grid, RED_T, 0, s, a);
+    return launched();
+}
+
+lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
+                        size_t ws_bytes = 0) {
     // the widest load class that A's rows (base + lda) and x all allow; the order of the
     // arithmetic does not depend on it (gemv.cuh)
     const uintptr_t al = reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.x);
     const int lw = ((al & 31) == 0 && a.lda % 8 == 0) ? 8 : ((al & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
+    if (a.n >= GEMV_LONG_N) {  // long rows: the stand-alone dot's order (gemv_long.cuh)
+        // few rows cannot fill the GPU with one CTA each: split them over (row, chunk)
+        // CTAs when the caller gave a workspace large enough
+        const bool split = !a.y_peers && ws && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
+                           a.m < 4 * (int64_t)sm_count(current_device()) &&
+                           ws_bytes >= gemv_ws_bytes_for(a.m, a.n);
+        if (split)
+            return lw == 8 ? gemv_split_go<8>(a, ws, ws_bytes, s)
+                 : lw == 4 ? gemv_split_go<4>(a, ws, ws_bytes, s) : gemv_split_go<1>(a, ws, ws_bytes, s);
+        if (a.y_peers)
+            return lw == 8 ? gemv_long_go<8, true>(a, s)
+                 : lw == 4 ? gemv_long_go<4, true>(a, s) : gemv_long_go<1, true>(a, s);
+        return lw == 8 ? gemv_long_go<8, false>(a, s)
+             : lw == 4 ? gemv_long_go<4, false>(a, s) : gemv_long_go<1, false>(a, s);
+    }
     return a.y_peers ? gemv_trl<true>(a, lw, s) : gemv_trl<false>(a, lw, s);
 }
 
@@ -553,6 +606,30 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
     a.y_out = y_out;
     return gemv_launch(a, reinterpret_cast<cudaStream_t>(stream));
 }
+
+lift_status lift_gemv_ws(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
+                         const float* x, float beta, const float* y, float* y_out, void* ws,
+                         size_t ws_bytes, lift_stream_t stream) {
+    if (m < 0 || n < 0) return LIFT_ERR_INVALID_VALUE;
+    if (lda < (n > 1 ? n : 1)) return LIFT_ERR_INVALID_VALUE;
+    if (m == 0) return LIFT_OK;
+    if (!y || !y_out || (n > 0 && (!A || !x))) return LIFT_ERR_NULL_POINTER;
+    if (misaligned4(A) || misaligned4(x) || misaligned4(y) || misaligned4(y_out))
+        return LIFT_ERR_INVALID_VALUE;
+    GemvArgs a{};
+    a.m = m;
+    a.n = n;
+    a.lda = lda;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.A = A;
+    a.x = x;
+    a.y = y;
+    a.y_out = y_out;
+    return gemv_launch(a, reinterpret_cast<cudaStream_t>(stream), ws, ws_bytes);
+}
+
+size_t lift_gemv_workspace_bytes(int64_t m, int64_t n) { return gemv_ws_bytes_for(m, n); }
 
 lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,
                               float* call, float* put, lift_stream_t stream) {

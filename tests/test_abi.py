@@ -104,6 +104,13 @@ def test_argument_errors_are_synchronous():
     assert lib.lift_gemv(0, 4, 1.0, None, 4, None, 1.0, None, None, None) == OK
     assert lib.lift_gemv(4, 4, 1.0, None, 4, p, 1.0, p, p, None) == NULLP
     assert lib.lift_gemv(4, 0, 1.0, None, 1, None, 1.0, None, p, None) == NULLP
+    # gemv with a workspace: same argument checks; the split workspace size
+    assert lib.lift_gemv_ws(-1, 4, 1.0, p, 4, p, 1.0, p, p, None, 0, None) == INVALID
+    assert lib.lift_gemv_ws(0, 4, 1.0, None, 4, None, 1.0, None, None, None, 0, None) == OK
+    assert lib.lift_gemv_workspace_bytes(3, 100) == 0
+    w1 = lib.lift_gemv_workspace_bytes(1, 1 << 16)
+    w3 = lib.lift_gemv_workspace_bytes(3, 1 << 24)
+    assert 0 < w1 < w3 and w3 % 16 == 0
     assert lib.lift_blackscholes(-1, p, 100.0, 0.05, 0.2, 1.0, p, p, None) == INVALID
     assert lib.lift_blackscholes(8, p, 0.0, 0.05, 0.2, 1.0, p, p, None) == INVALID   # K <= 0
     assert lib.lift_blackscholes(8, p, 100.0, 0.05, -0.2, 1.0, p, p, None) == INVALID

@@ -469,3 +469,37 @@ def test_reduce_order_depends_on_n_only(lift, n):
         assert np.array_equal(bits(lift.dot(dev(x), dev(y))), rd)
     finally:
         lift.set_grid_limit(0)
+
+
+# ------------------------------------------- gemv long rows (n >= 65536): the dot order
+@pytest.mark.parametrize("m,n", [(1, 1 << 16), (3, (1 << 20) + 5), (7, 200003), (40, 70000)])
+def test_gemv_long_rows_equal_dot_bits(lift, m, n):
+    A = rough(m * n, 11).reshape(m, n)
+    x = rough(n, 12)
+    y = rough(m, 13)
+    Ad, xd = dev(A), dev(x)
+    g = bits(lift.gemv(Ad, xd, dev(y), 1.0, 0.0))          # fp32(1 * d + 0 * y) = fp32(d)
+    d = np.concatenate([bits(lift.dot(Ad[i], xd)) for i in range(m)])
+    assert np.array_equal(g, d)
+    check_gemv(lift.gemv(Ad, xd, dev(y), -1.5, 0.25).cpu().numpy(), A, x, y, -1.5, 0.25)
+    # split path (workspace) == one CTA per row
+    assert np.array_equal(bits(lift.gemv(Ad, xd, dev(y), -1.5, 0.25)),
+                          bits(lift.gemv(Ad, xd, dev(y), -1.5, 0.25, split=False)))
+
+
+def test_gemv_long_rows_many_rows_and_ws_reuse(lift):
+    """Many long rows take the one-CTA-per-row kernel, a few take the split kernel: the
+    same rows give the same bits; the split workspace is reused across shapes."""
+    n = 65536 + 77
+    m = 700
+    A = dev(rough(m * n, 21).reshape(m, n))
+    x, y = dev(rough(n, 22)), dev(rough(m, 23))
+    full = bits(lift.gemv(A, x, y, 1.5, 0.5))
+    for a, b in [(0, 3), (5, 6), (600, 700), (1, 300)]:
+        assert np.array_equal(bits(lift.gemv(A[a:b], x, y[a:b], 1.5, 0.5)), full[a:b]), (a, b)
+    for _ in range(3):
+        assert np.array_equal(bits(lift.gemv(A[:2], x, y[:2], 1.5, 0.5)), full[:2])
+        xs = dev(rough(1 << 20, 24))
+        As = dev(rough(2 << 20, 25).reshape(2, 1 << 20))
+        s1 = bits(lift.gemv(As, xs, y[:2], 1.0, 0.0))
+        assert np.array_equal(s1, np.concatenate([bits(lift.dot(As[i], xs)) for i in range(2)]))
