@@ -38,5 +38,10 @@ for m, n, pad in [(3, 5, 0), (40, 1000, 3), (30, 3001, 1), (9, 4100, 0), (40, 81
                  (17, 9000, 4), (5, 20000, 0)]:
     A = torch.rand(m, n + pad, generator=g).to(dev)[:, :n]
     lift.gemv(A, rnd(n), rnd(m), 1.5, 0.5)
+# long rows: split path (few rows, workspace) twice (ticket reset), one CTA per row
+for m, n, split in [(2, 65536 + 5, True), (1, 1 << 19, True), (2, 65536 + 5, True),
+                    (3, 70001, False), (600, 65536, True)]:
+    A = torch.rand(m, n, generator=g).to(dev)
+    lift.gemv(A, rnd(n), rnd(m), 1.5, 0.5, split=split)
 torch.cuda.synchronize()
 print("sanitize probe ok")
