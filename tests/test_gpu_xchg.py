@@ -52,7 +52,7 @@ def _worker(rank, world, port, q):
         re = ex.asum(x if rank == 0 else e)
         out.append(re.cpu().numpy().view(np.uint32).tolist())
         # gemv with the y all-gather fused in (uneven row split, twice: both banks)
-        for m, k in [(1001, 777), (300, 8192)]:
+        for m, k in [(1001, 777), (300, 8192), (5, 70003)]:
             r0, r1 = ldist.row_range(m, rank, world)
             A = gen.fill_device(torch.empty((r1 - r0) * k, device=dev), 4, gen.TID_A, r0 * k)
             gx = gen.fill_device(torch.empty(k, device=dev), 4, gen.TID_X, 0)
@@ -99,13 +99,13 @@ def test_fused_exchange_two_processes_one_gpu():
         assert res[0][it][1] == lift.dot(x, y).cpu().numpy().view(np.uint32).tolist()
     x = gen.fill_device(torch.empty(1000, device=dev), 9, gen.TID_X, 0)
     assert res[0][5] == lift.asum(x).cpu().numpy().view(np.uint32).tolist()  # empty peer
-    for j, (m, k) in enumerate([(1001, 777), (300, 8192)]):  # fused all-gather == gemv
+    for j, (m, k) in enumerate([(1001, 777), (300, 8192), (5, 70003)]):  # fused all-gather == gemv
         A = gen.fill_device(torch.empty(m * k, device=dev), 4, gen.TID_A, 0).view(m, k)
         gx = gen.fill_device(torch.empty(k, device=dev), 4, gen.TID_X, 0)
         gy = gen.fill_device(torch.empty(m, device=dev), 4, gen.TID_Y, 0)
         full = lift.gemv(A, gx, gy, 1.5, 0.5).cpu().numpy().view(np.uint32).tolist()
         assert res[0][6 + j] == full and res[1][6 + j] == full
-    assert res[0][8] == 0 and res[1][8] == 0     # no timeouts
+    assert res[0][9] == 0 and res[1][9] == 0     # no timeouts
 
 
 def test_fused_exchange_single_rank():
