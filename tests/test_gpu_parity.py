@@ -503,3 +503,29 @@ def test_gemv_long_rows_many_rows_and_ws_reuse(lift):
         As = dev(rough(2 << 20, 25).reshape(2, 1 << 20))
         s1 = bits(lift.gemv(As, xs, y[:2], 1.0, 0.0))
         assert np.array_equal(s1, np.concatenate([bits(lift.dot(As[i], xs)) for i in range(2)]))
+
+
+@pytest.mark.parametrize("n", [5, 24, 300, 3001, 8192 + 3, 70001])
+def test_gemv_special_values_stay_in_their_row(lift, n):
+    """NaN / Inf placed at the first column, the last column (the masked last batch or the
+    partial last vector) and mid-row reach exactly their own row, for every threads-per-row
+    class and the long-row path; Inf x 0 gives NaN as in the oracle."""
+    m = 9
+    A, x, y = gemv_inputs(m, n, 123)
+    A = A.copy()
+    x = x.copy()
+    A[1, 0] = np.nan
+    A[3, n - 1] = np.inf
+    A[5, n // 2] = -np.inf
+    A[7, n - 1] = np.inf
+    x[n - 1] = 0.0 if n > 1 else x[n - 1]   # row 7: Inf * 0 = NaN; row 3 too
+    got = lift.gemv(dev(A), dev(x), dev(y), 1.5, 0.5).cpu().numpy()
+    ref = oracle.gemv(A, x, y, 1.5, 0.5).astype(np.float32)
+    for i in range(m):
+        if np.isnan(ref[i]):
+            assert np.isnan(got[i]), i
+        elif np.isinf(ref[i]):
+            assert got[i] == ref[i], i
+        else:
+            assert np.isfinite(got[i]) and abs(got[i] - ref[i]) <= 1e-6 * abs(ref[i]), i
+    assert np.isnan(got[1]) and np.isinf(got[5]) and got[5] < 0
