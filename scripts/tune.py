@@ -34,6 +34,12 @@ SPACE = {
                ("g_b8m2", "-DLIFT_GEMV_B=8 -DLIFT_GEMV_MINB=2"),
                ("g_b4m3", "-DLIFT_GEMV_B=4 -DLIFT_GEMV_MINB=3")],
     "grid": [("nonpersistent", "-DLIFT_PERSISTENT=0"), ("persistent", "-DLIFT_PERSISTENT=1")],
+    "scal_tile": [("s1024x1", "-DLIFT_SCAL_T=1024 -DLIFT_SCAL_U=1"),
+                  ("s512x1", "-DLIFT_SCAL_T=512 -DLIFT_SCAL_U=1"),
+                  ("s256x2", "-DLIFT_SCAL_T=256 -DLIFT_SCAL_U=2"),
+                  ("s256x4", "-DLIFT_SCAL_T=256 -DLIFT_SCAL_U=4")],
+    "pdl": [("pdl_on", "-DLIFT_PDL=1"), ("pdl_off", "-DLIFT_PDL=0")],
+    "ticket_fence": [("acq_rel", "-DLIFT_SC_FENCE=0"), ("sc_fence", "-DLIFT_SC_FENCE=1")],
 }
 
 
