@@ -269,6 +269,10 @@ const void* scal_fn(bool alias) {
     return alias ? (const void*)scal_kernel<LW, true> : (const void*)scal_kernel<LW, false>;
 }
 
+#ifndef LIFT_GEMV_REALIGN
+#define LIFT_GEMV_REALIGN 1  // misaligned rows: realigned 256-bit loads + lane shuffles
+#endif
+
 template <int TRL, int LW, bool PEERS>
 lift_status gemv_go(GemvArgs a, cudaStream_t s) {
     constexpr int64_t rp = GEMV_T >> TRL;  // rows per block
@@ -281,6 +285,7 @@ lift_status gemv_go(GemvArgs a, cudaStream_t s) {
 
 template <int TRL, bool PEERS>
 lift_status gemv_lw(const GemvArgs& a, int lw, cudaStream_t s) {
+    if (lw == 2) return gemv_go<TRL, 2, PEERS>(a, s);
     return lw == 8 ? gemv_go<TRL, 8, PEERS>(a, s)
          : lw == 4 ? gemv_go<TRL, 4, PEERS>(a, s) : gemv_go<TRL, 1, PEERS>(a, s);
 }
@@ -341,7 +346,7 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
     // the widest load class that A's rows (base + lda) and x all allow; the order of the
     // arithmetic does not depend on it (gemv.cuh)
     const uintptr_t al = reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.x);
-    const int lw = ((al & 31) == 0 && a.lda % 8 == 0) ? 8 : ((al & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
+    int lw = ((al & 31) == 0 && a.lda % 8 == 0) ? 8 : ((al & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
     if (a.n >= GEMV_LONG_N) {  // long rows: the stand-alone dot's order (gemv_long.cuh)
         // few rows cannot fill the GPU with one CTA each: split them over (row, chunk)
         // CTAs when the caller gave a workspace large enough
@@ -357,6 +362,8 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
         return lw == 8 ? gemv_long_go<8, false>(a, s)
              : lw == 4 ? gemv_long_go<4, false>(a, s) : gemv_long_go<1, false>(a, s);
     }
+    // rows at arbitrary 4-byte alignment with x 32-byte aligned: realigned 256-bit loads
+    if (lw == 1 && (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && LIFT_GEMV_REALIGN) lw = 2;
     return a.y_peers ? gemv_trl<true>(a, lw, s) : gemv_trl<false>(a, lw, s);
 }
 
