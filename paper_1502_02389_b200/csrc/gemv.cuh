@@ -131,45 +131,6 @@ __device__ __forceinline__ void gemv_block_done(const GemvArgs& a) {
 // TRL = log2(threads per row) = gemv_tr_log2(n); LW = load width class of A, lda and x;
 // PEERS = the NEXT-1 fused all-gather (its code in the block loop costs the plain kernel
 // ~20% through worse load scheduling, so it is a separate instantiation).
-// LW == 2: rows at any 4-byte alignment (odd n with lda = n, offset views), x 32-byte
-// aligned.  A lane loads the 32-byte-aligned block holding the start of its vector and
-// the following block (through L1, where it is usually the next lane's block) and shifts
-// by d = the row's offset in floats past a 32-byte boundary.  The values, hence the
-// order, are those of any other load width.  (Taking the next block from lane + 1 by
-// shuffle measured slower: 72.9 vs 63.2 us at 8192 x 8191.)
-template <int D>
-__device__ __forceinline__ f8 realign(const f8& own, const f8& nxt) {
-    f8 v;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v.v[e] = (e + D < 8) ? own.v[e + D] : nxt.v[e + D - 8];
-    return v;
-}
-
-// own = the 32-byte block at pa + 8q; nxt = the next block (from lane + 1, or loaded by
-// the warp's last lane); d = the row's offset past the 32-byte boundary (warp-uniform).
-__device__ __forceinline__ f8 ld_l1_v8(const float* p) {  // read-only, L1-allocating
-    f8 r;
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
-          "=f"(r.v[6]), "=f"(r.v[7])
-        : "l"(p));
-    return r;
-}
-
-__device__ __forceinline__ f8 realign_rt(const f8& own, const float* pa, int64_t q, int d) {
-    const f8 nxt = ld_l1_v8(pa + 8 * (q + 1));  // mostly an L1 hit: the next lane's block
-    switch (d) {  // uniform per row
-        case 1: return realign<1>(own, nxt);
-        case 2: return realign<2>(own, nxt);
-        case 3: return realign<3>(own, nxt);
-        case 4: return realign<4>(own, nxt);
-        case 5: return realign<5>(own, nxt);
-        case 6: return realign<6>(own, nxt);
-        case 7: return realign<7>(own, nxt);
-        default: return own;
-    }
-}
-
 // One row's slot accumulators (thread tp of TR): the canonical order of gemv.cuh.
 template <int TRL, int LW>
 __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp, int tp, int lane,
@@ -177,7 +138,6 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
     constexpr int TR = 1 << TRL;
     constexpr int B = LW == 2 ? 2 : GEMV_B;  // realigned rows: 2 (4 spills or interleaves; measured)
     const int d = LW == 2 ? (int)((reinterpret_cast<uintptr_t>(rp) >> 2) & 7) : 0;
-    const float* pa = rp - d;  // 32-byte aligned when LW == 2
     constexpr int LX = LW == 2 ? 8 : LW;  // x: 32-byte aligned on the realigned path
     int64_t k = 0;
     for (; (k + B) * TR <= nv; k += B) {  // full batches: every vector in range
@@ -185,12 +145,9 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             const int64_t q = tp + (k + b) * TR;
-            av[b] = LW == 2 ? ld_l1_v8(pa + 8 * q) : ld_slot<LW == 2 ? 8 : LW>(rp + 8 * q);
+            av[b] = LW == 2 ? ld_realigned(rp + 8 * q, d, q > 0 && 8 * q - d + 16 <= a.n)
+                            : ld_slot<LW == 2 ? 8 : LW>(rp + 8 * q);
             xv[b] = ld_x<LX>(a.x + 8 * q);
-        }
-        if constexpr (LW == 2) {
-#pragma unroll
-            for (int b = 0; b < B; ++b) av[b] = realign_rt(av[b], pa, tp + (k + b) * TR, d);
         }
 #pragma unroll
         for (int b = 0; b < B; ++b)
@@ -205,8 +162,8 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
             const int64_t q0 = tp + (k + b) * TR;
             const bool in = q0 < nv;
             const int64_t q = in ? q0 : nv - 1;  // a valid address; the value is masked
-            av[b] = LW == 2 ? ld_l1_v8(pa + 8 * q) : ld_slot<LW == 2 ? 8 : LW>(rp + 8 * q);
-            if constexpr (LW == 2) av[b] = realign_rt(av[b], pa, q, d);
+            av[b] = LW == 2 ? ld_realigned(rp + 8 * q, d, q > 0 && 8 * q - d + 16 <= a.n)
+                            : ld_slot<LW == 2 ? 8 : LW>(rp + 8 * q);
             xv[b] = ld_x<LX>(a.x + 8 * q);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {

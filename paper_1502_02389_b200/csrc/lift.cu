@@ -186,6 +186,10 @@ struct XchgArgs {  // NEXT-1: in-kernel cross-GPU combine (all null: single GPU)
     int* error = nullptr;
 };
 
+#ifndef LIFT_REDUCE_REALIGN
+#define LIFT_REDUCE_REALIGN 1  // 4-byte-aligned asum/dot operands: realigned 256-bit loads
+#endif
+
 template <class Op, int B>
 lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out32, double* out64,
                           void* ws, size_t ws_bytes, cudaStream_t stream, float alpha = 0.f,
@@ -243,13 +247,18 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     uintptr_t al = reinterpret_cast<uintptr_t>(x);
     if (Op::kTwoInputs) al |= reinterpret_cast<uintptr_t>(y);
     if (Op::kMapStore) al |= reinterpret_cast<uintptr_t>(map_out);
-    const int lw = align_class(al);
+    int lw = align_class(al);
+    if constexpr (!Op::kMapStore) {
+        if (lw == 1 && LIFT_REDUCE_REALIGN) lw = 2;  // realigned 256-bit blocks (common.cuh)
+    }
     const void* fn = lw == 8 ? (const void*)reduce_kernel<Op, 8, B>
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
+                   : lw == 2 ? (const void*)reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>
                              : (const void*)reduce_kernel<Op, 1, B>;
     const int64_t grid = grid_for(L.nc, fn, RED_T, 0, LIFT_PERSISTENT);
     if (lw == 8) launch(reduce_kernel<Op, 8, B>, grid, RED_T, 0, stream, a);
     else if (lw == 4) launch(reduce_kernel<Op, 4, B>, grid, RED_T, 0, stream, a);
+    else if (lw == 2) launch(reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>, grid, RED_T, 0, stream, a);
     else launch(reduce_kernel<Op, 1, B>, grid, RED_T, 0, stream, a);
     return launched();
 }

@@ -39,6 +39,9 @@
 
 namespace lift {
 
+#ifndef LIFT_RED_RB
+#define LIFT_RED_RB 2
+#endif
 #ifndef LIFT_SC_FENCE
 #define LIFT_SC_FENCE 0
 #endif
@@ -228,22 +231,38 @@ __global__ void xchg_only_kernel(ReduceArgs a) {
     if (threadIdx.x < 32) xchg_combine(a, 0.0);
 }
 
+// LW == 2: operands at any 4-byte alignment (slices at odd float offsets), read as
+// 32-byte-aligned blocks and shifted (common.cuh ld_realigned); never with a map store.
 template <class Op, int LW, int B0>
 __device__ __forceinline__ void chunk_body_full(const float* xc, const float* yc,
                                                 typename Op::acc_t* acc, float alpha = 0.f,
-                                                float* mo = nullptr) {
-    constexpr int B = B0 < RED_K ? B0 : RED_K;
+                                                float* mo = nullptr, int64_t base = 0,
+                                                int64_t n = 0) {
+    constexpr int BL = LW == 2 ? LIFT_RED_RB : B0;  // realigned: fewer vectors held (registers)
+    constexpr int B = BL < RED_K ? BL : RED_K;
     static_assert(RED_K % B == 0, "load batch must divide RED_K");
+    static_assert(LW != 2 || !Op::kMapStore, "no realigned map stores");
     const int t = threadIdx.x;
+    // LW == 2: offsets past a 32-byte boundary (uniform); base, n: this chunk's first global
+    // element and the operand length, for ld_realigned's inside-the-operand test
+    const int dx = LW == 2 ? (int)((reinterpret_cast<uintptr_t>(xc) >> 2) & 7) : 0;
+    const int dy = (LW == 2 && Op::kTwoInputs) ? (int)((reinterpret_cast<uintptr_t>(yc) >> 2) & 7) : 0;
 #pragma unroll
     for (int k0 = 0; k0 < RED_K; k0 += B) {
         f8 xv[B];
         f8 yv[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-            xv[b] = ld_slot<LW>(xc + (int64_t)RED_V * (t + (k0 + b) * RED_T));
-            if constexpr (Op::kTwoInputs)
-                yv[b] = ld_slot<LW>(yc + (int64_t)RED_V * (t + (k0 + b) * RED_T));
+            const int64_t q = t + (k0 + b) * RED_T;
+            if constexpr (LW == 2) {
+                const int64_t j = base + (int64_t)RED_V * q;  // global index of the vector
+                xv[b] = ld_realigned(xc + (int64_t)RED_V * q, dx, j >= dx && j - dx + 16 <= n);
+                if constexpr (Op::kTwoInputs)
+                    yv[b] = ld_realigned(yc + (int64_t)RED_V * q, dy, j >= dy && j - dy + 16 <= n);
+            } else {
+                xv[b] = ld_slot<LW>(xc + (int64_t)RED_V * q);
+                if constexpr (Op::kTwoInputs) yv[b] = ld_slot<LW>(yc + (int64_t)RED_V * q);
+            }
         }
         if constexpr (Op::kMapStore) {
 #pragma unroll
@@ -333,7 +352,7 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
                                                 min((int64_t)RED_C, a.n - base), acc64);
             } else {
                 using Op64 = typename Op::template rebind<double>;
-                if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64);
+                if (full) chunk_body_full<Op64, LW, B>(xc, yc, acc64, 0.f, nullptr, base, a.n);
                 else chunk_body_tail<Op64>(xc, yc, a.n - base, acc64);
             }
             wv = warp_pairwise(pairwise8(acc64));
@@ -420,7 +439,7 @@ __global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArg
 #pragma unroll
         for (int e = 0; e < RED_V; ++e) acc[e] = 0;
         float* mo = Op::kMapStore ? a.map_out + base : nullptr;
-        if (base + RED_C <= a.n) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo);
+        if (base + RED_C <= a.n) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo, base, a.n);
         else chunk_body_tail<Op>(xc, yc, a.n - base, acc, a.alpha, mo);
         chunk_finish<Op, LW, B>(a, c, acc, wbuf, parity);
     }
