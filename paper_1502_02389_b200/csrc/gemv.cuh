@@ -136,18 +136,22 @@ template <int TRL, int LW>
 __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp, int tp, int lane,
                                              int64_t nv, int tailn, double (&acc)[8]) {
     constexpr int TR = 1 << TRL;
-    constexpr int B = LW == 2 ? 2 : GEMV_B;  // realigned rows: 2 (4 spills or interleaves; measured)
-    const int d = LW == 2 ? (int)((reinterpret_cast<uintptr_t>(rp) >> 2) & 7) : 0;
-    constexpr int LX = LW == 2 ? 8 : LW;  // x: 32-byte aligned on the realigned path
+    constexpr int B = (LW == 2 || LW == 3) ? 2 : GEMV_B;  // realigned rows: 2 (4 spills; measured)
+    const int d = (LW == 2 || LW == 3) ? (int)((reinterpret_cast<uintptr_t>(rp) >> 2) & 7) : 0;
+    // LW 2: rows realigned, x 32-byte aligned; LW 3: rows and x realigned
+    constexpr bool RA = LW == 2 || LW == 3;
+    constexpr int LX = RA ? 8 : LW;
+    const int dxo = LW == 3 ? (int)((reinterpret_cast<uintptr_t>(a.x) >> 2) & 7) : 0;
     int64_t k = 0;
     for (; (k + B) * TR <= nv; k += B) {  // full batches: every vector in range
         f8 av[B], xv[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
             const int64_t q = tp + (k + b) * TR;
-            av[b] = LW == 2 ? ld_realigned(rp + 8 * q, d, q > 0 && 8 * q - d + 16 <= a.n)
-                            : ld_slot<LW == 2 ? 8 : LW>(rp + 8 * q);
-            xv[b] = ld_x<LX>(a.x + 8 * q);
+            av[b] = RA ? ld_realigned(rp + 8 * q, d, q > 0 && 8 * q - d + 16 <= a.n)
+                       : ld_slot<RA ? 8 : LW>(rp + 8 * q);
+            xv[b] = LW == 3 ? ld_realigned(a.x + 8 * q, dxo, q > 0 && 8 * q - dxo + 16 <= a.n)
+                            : ld_x<LX>(a.x + 8 * q);
         }
 #pragma unroll
         for (int b = 0; b < B; ++b)
@@ -162,9 +166,10 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
             const int64_t q0 = tp + (k + b) * TR;
             const bool in = q0 < nv;
             const int64_t q = in ? q0 : nv - 1;  // a valid address; the value is masked
-            av[b] = LW == 2 ? ld_realigned(rp + 8 * q, d, q > 0 && 8 * q - d + 16 <= a.n)
-                            : ld_slot<LW == 2 ? 8 : LW>(rp + 8 * q);
-            xv[b] = ld_x<LX>(a.x + 8 * q);
+            av[b] = RA ? ld_realigned(rp + 8 * q, d, q > 0 && 8 * q - d + 16 <= a.n)
+                       : ld_slot<RA ? 8 : LW>(rp + 8 * q);
+            xv[b] = LW == 3 ? ld_realigned(a.x + 8 * q, dxo, q > 0 && 8 * q - dxo + 16 <= a.n)
+                            : ld_x<LX>(a.x + 8 * q);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 av[b].v[e] = in ? av[b].v[e] : 0.f;

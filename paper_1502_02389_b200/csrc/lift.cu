@@ -295,6 +295,7 @@ lift_status gemv_go(GemvArgs a, cudaStream_t s) {
 template <int TRL, bool PEERS>
 lift_status gemv_lw(const GemvArgs& a, int lw, cudaStream_t s) {
     if (lw == 2) return gemv_go<TRL, 2, PEERS>(a, s);
+    if (lw == 3) return gemv_go<TRL, 3, PEERS>(a, s);
     return lw == 8 ? gemv_go<TRL, 8, PEERS>(a, s)
          : lw == 4 ? gemv_go<TRL, 4, PEERS>(a, s) : gemv_go<TRL, 1, PEERS>(a, s);
 }
@@ -371,8 +372,9 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
         return lw == 8 ? gemv_long_go<8, false>(a, s)
              : lw == 4 ? gemv_long_go<4, false>(a, s) : gemv_long_go<1, false>(a, s);
     }
-    // rows at arbitrary 4-byte alignment with x 32-byte aligned: realigned 256-bit loads
-    if (lw == 1 && (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 && LIFT_GEMV_REALIGN) lw = 2;
+    // rows and/or x at arbitrary 4-byte alignment: realigned 256-bit loads (common.cuh);
+    // 2 = rows only (x 32-byte aligned), 3 = rows and x
+    if (lw == 1 && LIFT_GEMV_REALIGN) lw = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 ? 2 : 3;
     return a.y_peers ? gemv_trl<true>(a, lw, s) : gemv_trl<false>(a, lw, s);
 }
 
