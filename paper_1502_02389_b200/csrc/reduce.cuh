@@ -39,6 +39,9 @@
 
 namespace lift {
 
+#ifndef LIFT_RED_RMINB
+#define LIFT_RED_RMINB 4  // resident CTAs per SM for the realigned (LW 2) reductions
+#endif
 #ifndef LIFT_RED_RB
 #define LIFT_RED_RB 2
 #endif
@@ -424,7 +427,7 @@ __device__ __forceinline__ void trace_start(int64_t c) {
 
 // One CTA per chunk, hardware-scheduled (the default).
 template <class Op, int LW, int B>
-__global__ void __launch_bounds__(RED_T, Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
+__global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
     pdl_wait();
     pdl_trigger();
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
