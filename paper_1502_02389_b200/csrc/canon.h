@@ -23,7 +23,7 @@ static_assert(RED_G <= RED_T, "group fold uses one leaf per thread");
 
 // gemv: rows of n >= GEMV_LONG_N = 65536 use exactly the dot order above (gemv_long.cuh);
 // shorter rows the order defined in gemv.cuh: TR = gemv_tr_log2(n) threads per row
-// (256 for n >= 8192, halving down to 1 for n <= 24), thread t' owns the 8-float
+// (128 at n = 8192, 256 from n = 16384, down to 1 for short rows), thread t' owns the 8-float
 // vectors t' + TR*k, 8 fp64 slot accumulators in ascending k, pairwise8, butterfly over
 // the row's lanes, the row's TR/32 warp values pairwise (TR > 32).
 
