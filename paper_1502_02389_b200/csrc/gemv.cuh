@@ -22,14 +22,14 @@
 //     (n % 8 != 0) is the last vector of its owner; thread value = pairwise fold of the
 //     8 accumulators; butterfly over the row's lanes (xor 1..min(TR,32)/2); for TR > 32
 //     the row's TR/32 warp values pairwise.
-//     Each thread keeps GEMV_B = 4 vectors (32 KiB per CTA) of A in flight.
+//     Each thread loads GEMV_B = 4 vectors of A per batch (32 KiB per CTA).
 //  G3 fused epilogue (rule 5f map-map fusion): y_out_i = fp32(fma(alpha, d_i,
 //     beta * y_i)) in fp64, rounded once (reading R10).  y_out may alias y.
 //
-// Why one CTA per row (n >= 8192) rather than one warp per row: a whole 32 KiB row is
+// Why a CTA (or half of one) per row rather than one warp per row: a whole 32 KiB row is
 // an ~11 us task for a single warp at its share of HBM bandwidth, so the last wave of
 // rows left SMs idle (the time stepped by ~9 us per extra wave, scripts/gemv_msweep.py);
-// a CTA finishes a row in ~2-3 us, and the hardware balances ~14 CTAs per resident slot.
+// 128-256 threads finish a row in a few us, and the hardware balances many CTAs per slot.
 //
 // The order of every addition is a function of n only (not of m, the grid, the load
 // width or alignment), so a row's bits are the same however rows are sharded.
