@@ -529,3 +529,20 @@ def test_gemv_special_values_stay_in_their_row(lift, n):
         else:
             assert np.isfinite(got[i]) and abs(got[i] - ref[i]) <= 1e-6 * abs(ref[i]), i
     assert np.isnan(got[1]) and np.isinf(got[5]) and got[5] < 0
+
+
+def test_gemv_ws_too_small_or_null_falls_back_with_same_bits(lift):
+    """lift_gemv_ws contract: a NULL or too-small workspace selects one CTA per row."""
+    from paper_1502_02389_b200._lib import lib
+    m, n = 3, 70001
+    A = dev(rough(m * n, 31).reshape(m, n))
+    x, y = dev(rough(n, 32)), dev(rough(m, 33))
+    want = bits(lift.gemv(A, x, y, 1.5, 0.5))
+    stream = torch.cuda.current_stream().cuda_stream
+    small = torch.zeros(64, dtype=torch.uint8, device=DEV)
+    for wp, wb in [(None, 0), (small.data_ptr(), small.numel())]:
+        out = torch.full((m,), float("nan"), device=DEV)
+        assert lib.lift_gemv_ws(m, n, 1.5, A.data_ptr(), n, x.data_ptr(), 0.5, y.data_ptr(),
+                                out.data_ptr(), wp, wb, stream) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(out), want)
