@@ -410,6 +410,12 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
         if (a.out_f64) *a.out_f64 = total;
         if (a.out_f32) *a.out_f32 = __double2float_rn(total);
     }
+#ifdef LIFT_TRACE
+    if (lane == 0) {  // timeline marker: the final result store (two-level path)
+        g_trace[3 * 65535] = gtimer();
+        g_trace[3 * 65535 + 1] = (unsigned long long)c;
+    }
+#endif
 }
 
 __device__ __forceinline__ void trace_start(int64_t c) {
