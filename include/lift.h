@@ -197,8 +197,9 @@ lift_status lift_gemv(int64_t m, int64_t n, float alpha, const float* A, int64_t
 lift_status lift_gemv_ws(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
                          const float* x, float beta, const float* y, float* y_out, void* ws,
                          size_t ws_bytes, lift_stream_t stream);
-/* Workspace bytes for lift_gemv_ws's split path at (m, n); 0 when rows are shorter than
- *   65536 columns (no split path). */
+/* Workspace bytes for lift_gemv_ws's split path at (m, n); 0 when no split would be used:
+ *   rows shorter than 65536 columns, or m >= 4 x the current device's SM count (one CTA
+ *   per row then fills the GPU). */
 size_t lift_gemv_workspace_bytes(int64_t m, int64_t n);
 
 /* NEXT-3 — BlackScholes (Fig. 9): map(BSComputation, s) over n stock prices.

@@ -647,7 +647,11 @@ lift_status lift_gemv_ws(int64_t m, int64_t n, float alpha, const float* A, int6
     return gemv_launch(a, reinterpret_cast<cudaStream_t>(stream), ws, ws_bytes);
 }
 
-size_t lift_gemv_workspace_bytes(int64_t m, int64_t n) { return gemv_ws_bytes_for(m, n); }
+size_t lift_gemv_workspace_bytes(int64_t m, int64_t n) {
+    // the split path is only taken for rows too few to fill the GPU (gemv_launch)
+    if (m >= 4 * (int64_t)sm_count(current_device())) return 0;
+    return gemv_ws_bytes_for(m, n);
+}
 
 lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,
                               float* call, float* put, lift_stream_t stream) {

@@ -111,6 +111,7 @@ def test_argument_errors_are_synchronous():
     w1 = lib.lift_gemv_workspace_bytes(1, 1 << 16)
     w3 = lib.lift_gemv_workspace_bytes(3, 1 << 24)
     assert 0 < w1 < w3 and w3 % 16 == 0
+    assert lib.lift_gemv_workspace_bytes(1 << 20, 1 << 16) == 0  # enough rows: no split
     assert lib.lift_blackscholes(-1, p, 100.0, 0.05, 0.2, 1.0, p, p, None) == INVALID
     assert lib.lift_blackscholes(8, p, 0.0, 0.05, 0.2, 1.0, p, p, None) == INVALID   # K <= 0
     assert lib.lift_blackscholes(8, p, 100.0, 0.05, -0.2, 1.0, p, p, None) == INVALID
