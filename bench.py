@@ -453,6 +453,9 @@ def run_lift(args):
         }
         if not args.no_extras:
             line["next_rows"] = next_rows(lift, gen, torch, dev, stream, x_v, y_v, r_asum, ws_a)
+            if world == 1:
+                line["baseline_configs"] = baseline_configs(lift, gen, torch, dev, x_v, y_v, x_d, y_d,
+                                                            A, g_x, g_y, g_out)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_budget)
         print(json.dumps(line), flush=True)
@@ -462,6 +465,68 @@ def run_lift(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def baseline_configs(lift, gen, torch, dev, x_v, y_v, x_d, y_d, A, g_x, g_y, g_out, reps=20):
+    """BASELINE.json's configs C1-C5 on this GPU, each alone: `reps` back-to-back launches in
+    one CUDA graph (median of 5 replays), reusing the step's operands where they match.
+    Operands >= 256 MiB exceed the 126 MB L2; C1 (4 MiB) is L2-resident by nature."""
+    cs = torch.cuda.Stream(device=dev)
+
+    def timed(fn, nbytes, n_reps=reps):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(cs):
+            fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs):
+                for _ in range(n_reps):
+                    fn()
+            ts = []
+            for _ in range(5):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(cs)
+                g.replay()
+                e.record(cs)
+                e.synchronize()
+                ts.append(s.elapsed_time(e) / n_reps * 1e3)
+        us = sorted(ts)[2]
+        gbs = nbytes / (us * 1e-6) / 1e9
+        return {"us": round(us, 2), "GB/s": round(gbs, 1), "frac_8TBs": round(gbs / NOMINAL_HBM, 3)}
+
+    r = torch.empty(1, dtype=torch.float32, device=dev)
+    ws = lift.Workspace(1 << 28, dev)
+    out = {"note": "each config alone, CUDA-graph back-to-back launches, median of 5"}
+    out["C1 asum 2^20 (L2-resident)"] = timed(lambda: lift.asum(x_v[:1 << 20], out=r, ws=ws), 4 << 20)
+    # C2: 2^24 rotates over 4 disjoint slices of the step's operands (so it streams HBM)
+    k = [0]
+
+    def dot24():
+        i = k[0] % 4
+        k[0] += 1
+        lift.dot(x_v[i << 24:(i + 1) << 24], y_v[i << 24:(i + 1) << 24], out=r, ws=ws)
+    y_v.copy_(x_v)
+    out["C2 dot 2^24"] = timed(dot24, 8 << 24)
+    out["C2 dot 2^26"] = timed(lambda: lift.dot(x_d, y_d, out=r, ws=ws), 8 << 26)
+    out["C3 scal 2^28"] = timed(lambda: lift.scal(ALPHA_SCAL, x_v, out=y_v), 8 << 28)
+    out["C3 asum 2^28"] = timed(lambda: lift.asum(x_v, out=r, ws=ws), 4 << 28)
+    m, n = A.shape
+    out["C4 gemv 8192x8192 (p=1)"] = timed(lambda: lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out),
+                                           4 * (m * n + n + 2 * m))
+    sh = m // 8
+    out["C4 gemv 1024x8192 (one p=8 shard, L2-warm)"] = timed(
+        lambda: lift.gemv(A[:sh], g_x, g_y[:sh], ALPHA, BETA, out=g_out[:sh]), 4 * (sh * n + n + 2 * sh))
+    # C5: dot over 2^31 elements (16 GiB of inputs) on this one GPU, if memory allows
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free > (20 << 30):
+        bx = gen.fill_device(torch.empty(1 << 31, dtype=torch.float32, device=dev), 0, gen.TID_X, 0,
+                             gen.DIST_UNIFORM, 0.0, 1.0)
+        by = gen.fill_device(torch.empty(1 << 31, dtype=torch.float32, device=dev), 0, gen.TID_Y, 0,
+                             gen.DIST_UNIFORM, 0.0, 2.0)
+        wsb = lift.Workspace(1 << 31, dev)
+        out["C5 dot 2^31 (p=1)"] = timed(lambda: lift.dot(bx, by, out=r, ws=wsb), 8 << 31, n_reps=5)
+        del bx, by, wsb
+    return out
 
 
 def next_rows(lift, gen, torch, dev, stream, x_v, y_v, r, ws, reps=20):
