@@ -214,6 +214,28 @@ size_t lift_gemv_workspace_bytes(int64_t m, int64_t n);
 lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,
                               float* call, float* put, lift_stream_t stream);
 
+/* NEXT-4 — device-specific strategy variants, the analogs of the paper's per-device
+ *   lowerings (Fig. 7a/7b: tree in local memory or not, vector width, split
+ *   sizes), selectable at run time.  Every variant computes the SAME canonical order, so
+ *   none changes a result bit (tested); they only change how data moves.  Process-global;
+ *   value 0 = the tuned default.  Unknown knob or value: LIFT_ERR_INVALID_VALUE.
+ *     LIFT_VAR_LOAD_WIDTH  cap on the global load/store width: 0 auto (the widest the
+ *                          alignment allows: LDG/STG.256), 1 scalar, 4 = 128-bit, 8 = 256-bit
+ *     LIFT_VAR_GEMV_X      gemv rows of 2048..24576 columns: 0 auto, 1 x read through L1 and
+ *                          widened per use, 2 x staged once per CTA as fp64 in shared memory
+ *                          (persistent CTAs, Cluster Launch Control stealing)
+ *     LIFT_VAR_TREE        intra-warp tree of asum/dot/gemv: 0 auto (= 1), 1 shuffle
+ *                          butterfly, 2 shared-memory tree (iterate(split-2 reduce) in local
+ *                          memory, as the paper's Fig. 7a/7b) */
+typedef enum {
+    LIFT_VAR_LOAD_WIDTH = 0,
+    LIFT_VAR_GEMV_X = 1,
+    LIFT_VAR_TREE = 2,
+    LIFT_VAR_COUNT = 3
+} lift_variant;
+lift_status lift_set_variant(lift_variant knob, int value);
+int lift_get_variant(lift_variant knob);
+
 /* TEST HOOK: cap the number of CTAs any subsequent launch may use (0 = no cap,
  *   the default).  Used by the determinism tests to show results do not depend on
  *   the grid.  Process-global; not for production use. */

@@ -24,7 +24,8 @@ from ._lib import LiftError, check, lib
 
 __all__ = ["scal", "asum", "dot", "gemv", "asum_partial", "dot_partial", "combine", "blackscholes",
            "scal_asum",
-           "workspace_bytes", "Workspace", "LiftError", "set_grid_limit"]
+           "workspace_bytes", "Workspace", "LiftError", "set_grid_limit", "set_variant",
+           "get_variant", "VARIANTS"]
 
 
 def _stream_handle(device: torch.device) -> int:
@@ -105,6 +106,19 @@ def _workspace(n: int, device: torch.device) -> Workspace:
 def set_grid_limit(max_ctas: int) -> None:
     """Test hook (lift_debug_set_grid_limit): cap CTAs per launch; 0 = no cap."""
     check(lib.lift_debug_set_grid_limit(int(max_ctas)))
+
+
+#: NEXT-4 runtime strategy knobs (lift.h lift_variant); every value gives the same bits.
+VARIANTS = {"load_width": 0, "gemv_x": 1, "tree": 2}
+
+
+def set_variant(knob: str, value: int) -> None:
+    """Select a strategy variant (lift_set_variant); 0 restores the tuned default."""
+    check(lib.lift_set_variant(VARIANTS[knob], int(value)))
+
+
+def get_variant(knob: str) -> int:
+    return int(lib.lift_get_variant(VARIANTS[knob]))
 
 
 def scal(alpha: float, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

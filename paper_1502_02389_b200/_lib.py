@@ -19,7 +19,8 @@ EXPORTS = (
     "lift_reduce_group_chunks", "lift_blackscholes", "lift_scal_asum", "lift_xchg_bytes",
     "lift_xchg_create", "lift_xchg_destroy", "lift_ipc_get_handle", "lift_ipc_open_handle",
     "lift_ipc_close_handle", "lift_asum_allreduce", "lift_dot_allreduce", "lift_ipc_alloc",
-    "lift_gemv_allgather", "lift_gemv_ws", "lift_gemv_workspace_bytes",
+    "lift_gemv_allgather", "lift_gemv_ws", "lift_gemv_workspace_bytes", "lift_set_variant",
+    "lift_get_variant",
 )
 
 LIFT_OK = 0
@@ -48,6 +49,8 @@ def _load():
         "lift_gemv": ([_i64, _i64, _f32, _vp, _i64, _vp, _f32, _vp, _vp, _vp], _int),
         "lift_gemv_ws": ([_i64, _i64, _f32, _vp, _i64, _vp, _f32, _vp, _vp, _vp, _sz, _vp], _int),
         "lift_gemv_workspace_bytes": ([_i64, _i64], _sz),
+        "lift_set_variant": ([_int, _int], _int),
+        "lift_get_variant": ([_int], _int),
         "lift_debug_set_grid_limit": ([_int], _int),
         "lift_reduce_chunk_elems": ([], _i64),
         "lift_reduce_group_chunks": ([], _int),

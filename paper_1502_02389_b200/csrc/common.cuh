@@ -158,6 +158,74 @@ __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// ---- mbarrier + Cluster Launch Control (sm_100): hardware work stealing ---------------
+// A resident CTA cancels a not-yet-launched CTA of the same grid and takes over its
+// blockIdx (SASS UGETNEXTWORKID).  This gives persistent CTAs (per-CTA setup such as
+// gemv's x staging paid once per resident CTA) with the dynamic load balance of a
+// one-CTA-per-unit grid (per-SM bandwidth differs, so static splits finish unevenly).
+// Protocol: thread 0 issues clc_try_cancel before the current unit's work; after the
+// work every thread calls clc_fetch; a __syncthreads must separate clc_fetch from the
+// next clc_try_cancel (the response buffer is reused).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+struct Clc {
+    uint4* resp;    // 16-byte response, shared memory
+    uint64_t* bar;  // mbarrier (count 1), shared memory
+    uint32_t phase;
+};
+
+__device__ __forceinline__ void clc_try_cancel(const Clc& c) {
+    mbar_arrive_expect_tx(c.bar, 16);
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 "
+        "[%0], [%1];" ::"r"(smem_u32(c.resp)),
+        "r"(smem_u32(c.bar))
+        : "memory");
+}
+
+// Returns true and the stolen CTA's blockIdx.x in `next`, or false (no work left).
+__device__ __forceinline__ bool clc_fetch(Clc& c, int64_t& next) {
+    mbar_wait(c.bar, c.phase);
+    c.phase ^= 1u;
+    uint32_t ok, cx;
+    asm volatile(
+        "{ .reg .b128 r; .reg .pred p; ld.shared.b128 r, [%2]; "
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r; selp.u32 %0, 1, 0, p; "
+        "clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r; }"
+        : "=r"(ok), "=r"(cx)
+        : "r"(smem_u32(c.resp))
+        : "memory");
+    next = cx;
+    // order this generic read of the response before the next try_cancel's async write
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    return ok != 0;
+}
+
 // ---- NEXT-1 peer-memory exchange primitives (reduce.cuh, gemv.cuh) -----------------
 // Exchange buffer of one rank: [2 banks x p slots of XchgSlot][2 u64 counters].
 struct XchgSlot {

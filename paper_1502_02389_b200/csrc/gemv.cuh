@@ -42,6 +42,12 @@ namespace lift {
 #ifndef LIFT_GEMV_B
 #define LIFT_GEMV_B 4     // vectors per thread in flight (launch shape only, not the order)
 #endif
+#ifndef LIFT_GEMV_XJIT
+#define LIFT_GEMV_XJIT 0  // 1: a thread's A batch issued before any x load (x loaded per use)
+#endif
+#ifndef LIFT_GEMV_EXPT
+#define LIFT_GEMV_EXPT 0  // timing experiments only (scripts/gpu_r2_gemv.sh); never the product
+#endif
 #ifndef LIFT_GEMV_MINB
 #define LIFT_GEMV_MINB 4  // resident CTAs per SM: 64 registers, ~128 KiB of A in flight per SM
 #endif
@@ -78,6 +84,37 @@ __host__ __device__ constexpr int gemv_tr_log2(int64_t n) {
     return l;
 }
 
+// fp32 -> fp64 by integer ops (ALU pipe) — exact for normal numbers only (not 0, subnormal,
+// Inf, NaN); timing experiments (LIFT_GEMV_EXPT) only.
+__device__ __forceinline__ double f2d_bits(float f) {
+    const unsigned u = __float_as_uint(f);
+    const unsigned hi = (((u >> 3) & 0x0FFFFFFFu) | (u & 0x80000000u)) + 0x38000000u;
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+// Ordered (volatile) forms for LIFT_GEMV_XJIT: keep the A batch ahead of the x loads.
+template <int LW>
+__device__ __forceinline__ f8 ld_slot_vol(const float* p) {
+    if constexpr (LW == 8) {
+        f8 r;
+        asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                       "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                     : "l"(p));
+        return r;
+    } else {
+        return ld_slot<LW>(p);
+    }
+}
+__device__ __forceinline__ f8 ld_x_vol(const float* p) {
+    f8 r;
+    asm volatile("ld.global.nc.L1::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+
 // x through L1: one copy per SM serves every resident CTA (G1).
 template <int LW>
 __device__ __forceinline__ f8 ld_x(const float* p) {
@@ -103,19 +140,22 @@ __device__ __forceinline__ f8 ld_x(const float* p) {
     }
 }
 
-// NEXT-1 fused all-gather: after each row block the CTA counts it in this rank's
-// exchange buffer; the CTA that completes the LAST block publishes the rank's flag into
-// every peer's buffer (system-scope release; the row stores were fenced at system scope
-// before each count) and waits for all p flags, so the kernel ends only when every
-// rank's rows have landed in this rank's y — stream-ordered consumers can read it.
-__device__ __forceinline__ void gemv_block_done(const GemvArgs& a) {
+// NEXT-1 fused all-gather: a CTA counts the row blocks it finished in this rank's
+// exchange buffer (one system fence and one atomic per count; the persistent gemv_xs
+// kernel counts once per CTA, gemv_kernel once per block); the CTA that completes the
+// count publishes the rank's flag into every peer's buffer (system-scope release) and
+// waits for all p flags, so the kernel ends only when every rank's rows have landed in
+// this rank's y — stream-ordered consumers can read it.  Called by warp 0 after a CTA
+// barrier that follows the CTA's row stores.
+__device__ __forceinline__ void gemv_cta_done(const GemvArgs& a, int64_t count) {
     const int lane = threadIdx.x & 31;
     const int bank = (int)(a.epoch & 1ull);
     unsigned last = 0;
     if (lane == 0) {
-        __threadfence_system();  // this block's row stores (ordered by the barrier) before its count
+        __threadfence_system();  // the CTA's row stores (ordered by the barrier) before its count
         unsigned long long* cnt = xchg_counter(a.xpeers[a.rank], a.p, bank);
-        last = (atomicAdd(cnt, 1ull) == (unsigned long long)(a.nblocks - 1));
+        last = (atomicAdd(cnt, (unsigned long long)count) + (unsigned long long)count ==
+                (unsigned long long)a.nblocks);
         if (last) {
             __threadfence_system();
             *cnt = 0ull;  // reset for epoch + 2 (this bank's next use)
@@ -146,6 +186,24 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
     constexpr int LX = RA ? 8 : LW;
     const int dxo = LW == 3 ? (int)((reinterpret_cast<uintptr_t>(a.x) >> 2) & 7) : 0;
     int64_t k = 0;
+#if LIFT_GEMV_XJIT
+    if constexpr (!RA) {
+        // A batch first (all B loads in flight), then x just in time per vector (an L1
+        // hit), so x never holds registers across the DRAM wait
+        for (; (k + B) * TR <= nv; k += B) {
+            f8 av[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) av[b] = ld_slot_vol<LW>(rp + 8 * (tp + (k + b) * TR));
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const f8 xv = ld_x_vol(a.x + 8 * (tp + (k + b) * TR));
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    acc[e] = __fma_rn((double)av[b].v[e], (double)xv.v[e], acc[e]);
+            }
+        }
+    }
+#endif
     for (; (k + B) * TR <= nv; k += B) {  // full batches: every vector in range
         f8 av[B], xv[B];
 #pragma unroll
@@ -159,8 +217,22 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
 #pragma unroll
         for (int b = 0; b < B; ++b)
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < 8; ++e) {
+#if LIFT_GEMV_EXPT == 1  // TIMING EXPERIMENT ONLY (wrong results): no x conversion
+                acc[e] = __dadd_rn((double)av[b].v[e], acc[e]) + (double)__int_as_float(__float_as_int(xv[b].v[e]) & 0);
+#elif LIFT_GEMV_EXPT == 2  // TIMING EXPERIMENT: both widened by integer ops (normal numbers only)
+                acc[e] = __fma_rn(f2d_bits(av[b].v[e]), f2d_bits(xv[b].v[e]), acc[e]);
+#elif LIFT_GEMV_EXPT == 3  // TIMING EXPERIMENT: x widened by integer ops (normal numbers only)
+                acc[e] = __fma_rn((double)av[b].v[e], f2d_bits(xv[b].v[e]), acc[e]);
+#elif LIFT_GEMV_EXPT == 4  // TIMING EXPERIMENT: x loaded but not converted
+                acc[e] = __dadd_rn((double)av[b].v[e], acc[e]) + (xv[b].v[e] == 1234.5f ? 1.0 : 0.0);
+#elif LIFT_GEMV_EXPT == 6  // TIMING EXPERIMENT: x not loaded but converted (computed value)
+                acc[e] = __fma_rn((double)av[b].v[e],
+                                  (double)__int_as_float(0x3f800000 + (int)(k + b) * 8 + e + tp), acc[e]);
+#else
                 acc[e] = __fma_rn((double)av[b].v[e], (double)xv[b].v[e], acc[e]);
+#endif
+            }
     }
     if (k * TR < nv) {  // last batch: vectors >= nv are masked to +0 x +0
         f8 av[B], xv[B];
@@ -227,11 +299,14 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
             const double v = warp_pairwise(pairwise8(acc));
             if (lane == 0) wv[par][warp] = v;
             __syncthreads();
-            const double* w = wv[par] + (t >> 5);
-            if constexpr (TRL == 8) d = pairwise8(w);
-            else if constexpr (TRL == 7) d = __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3]));
-            else if constexpr (TRL == 6) d = __dadd_rn(w[0], w[1]);
-            else d = w[0];
+            d = 0.0;
+            if (tp == 0) {  // the row's TR/32 warps start at this thread's warp
+                const double* w = wv[par] + warp;
+                if constexpr (TRL == 8) d = pairwise8(w);
+                else if constexpr (TRL == 7) d = __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3]));
+                else if constexpr (TRL == 6) d = __dadd_rn(w[0], w[1]);
+                else d = w[0];
+            }
         }
         if (tp == 0 && live) {
             const double yb = __dmul_rn((double)a.beta, (double)a.y[row]);  // scal(b, y): exact
@@ -244,7 +319,7 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
         }
         if constexpr (PEERS) {
             __syncthreads();  // every row store of this block precedes its count
-            if (warp == 0) gemv_block_done(a);
+            if (warp == 0) gemv_cta_done(a, 1);
         }
     }
 }

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(RED_T, 4) gemv_long_kernel(GemvArgs a) {
         if (t == 0) gemv_row_out(a, row, ng > 1 ? gs.close() : gp, PEERS);
         if constexpr (PEERS) {
             __syncthreads();  // the row store precedes the block count
-            if (warp == 0) gemv_block_done(a);
+            if (warp == 0) gemv_cta_done(a, 1);
         }
     }
 }

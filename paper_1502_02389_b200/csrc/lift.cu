@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "blackscholes.cuh"
 #include "gemv.cuh"
+#include "gemv_xs.cuh"
 #include "reduce.cuh"
 #include "gemv_long.cuh"
 #include "scal.cuh"
@@ -53,6 +54,16 @@ __global__ void combine_kernel(int p, const double* __restrict__ partials, float
 namespace {
 
 std::atomic<int> g_grid_limit{0};
+std::atomic<int> g_var[LIFT_VAR_COUNT];  // NEXT-4 runtime variants (0 = tuned default)
+
+inline int var(lift_variant k) { return g_var[k].load(std::memory_order_relaxed); }
+
+// LIFT_VAR_LOAD_WIDTH: cap a load class (8 = 256-bit, 4 = 128-bit, 1 = scalar).
+inline int cap_lw(int lw) {
+    const int c = var(LIFT_VAR_LOAD_WIDTH);
+    return c == 0 ? lw : (lw < c ? lw : c);
+}
+inline bool lw_capped() { const int c = var(LIFT_VAR_LOAD_WIDTH); return c != 0 && c != 8; }
 
 std::atomic<int> g_sms[64];  // per-device SM count cache (0 = not yet queried)
 std::mutex g_mu;
@@ -90,10 +101,14 @@ int occupancy(const void* fn, int threads, size_t smem) {
     for (int i = 0; i < g_nocc; ++i)
         if (g_occ[i].fn == fn && g_occ[i].dev == dev && g_occ[i].smem == smem)
             return g_occ[i].blocks;
-    // The attribute is a per-function maximum: set it to the largest opt-in size once,
-    // so launches with any smaller dynamic smem (other n) stay valid.
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // The attribute is a per-function maximum: set it to the device's opt-in maximum, so
+    // launches with any dynamic smem size (other n) stay valid whatever the call order.
+    if (smem > 48 * 1024) {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin > (int)smem ? optin : (int)smem);
+    }
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess ||
         b < 1)
@@ -249,8 +264,10 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     if (Op::kMapStore) al |= reinterpret_cast<uintptr_t>(map_out);
     int lw = align_class(al);
     if constexpr (!Op::kMapStore) {
-        if (lw == 1 && LIFT_REDUCE_REALIGN) lw = 2;  // realigned 256-bit blocks (common.cuh)
+        // realigned 256-bit blocks (common.cuh); not when the variant caps the width
+        if (lw == 1 && LIFT_REDUCE_REALIGN && !lw_capped()) lw = 2;
     }
+    lw = lw == 2 ? 2 : cap_lw(lw);
     const void* fn = lw == 8 ? (const void*)reduce_kernel<Op, 8, B>
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
                    : lw == 2 ? (const void*)reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>
@@ -315,6 +332,33 @@ lift_status gemv_trl(const GemvArgs& a, int lw, cudaStream_t s) {
     }
 }
 
+#ifndef LIFT_GXS_AUTO
+#define LIFT_GXS_AUTO 0  // auto never picks the staged-x kernel: slower at every measured shape
+#endif                   // (DESIGN.md §6); LIFT_VAR_GEMV_X = 2 selects it
+inline bool gxs_auto(int64_t, int64_t) { return LIFT_GXS_AUTO != 0; }
+
+template <int TRL, int LW, bool PEERS>
+lift_status gxs_go(GemvArgs a, cudaStream_t s) {
+    constexpr int64_t rp = GXS_T >> TRL;  // rows per block
+    a.nblocks = (a.m + rp - 1) / rp;
+    const size_t smem = gxs_smem_bytes(a.n);
+    const void* fn = (const void*)gemv_xs_kernel<TRL, LW, PEERS>;
+    // CLC stealing: the grid covers every block (resident CTAs take the rest)
+    const int64_t grid = grid_for(a.nblocks, fn, GXS_T, smem, false, true);
+    launch(gemv_xs_kernel<TRL, LW, PEERS>, grid, GXS_T, smem, s, a);
+    return launched();
+}
+
+template <bool PEERS>
+lift_status gxs_trl(const GemvArgs& a, int lw, cudaStream_t s) {
+    switch (gemv_tr_log2(a.n)) {  // n >= GXS_NMIN: 32..256 threads per row
+        case 8: return lw == 8 ? gxs_go<8, 8, PEERS>(a, s) : gxs_go<8, 4, PEERS>(a, s);
+        case 7: return lw == 8 ? gxs_go<7, 8, PEERS>(a, s) : gxs_go<7, 4, PEERS>(a, s);
+        case 6: return lw == 8 ? gxs_go<6, 8, PEERS>(a, s) : gxs_go<6, 4, PEERS>(a, s);
+        default: return lw == 8 ? gxs_go<5, 8, PEERS>(a, s) : gxs_go<5, 4, PEERS>(a, s);
+    }
+}
+
 // Split-path workspace bytes for (m, n): partials + a ticket region of a third of W.
 size_t gemv_ws_bytes_for(int64_t m, int64_t n) {
     if (n < GEMV_LONG_N || m <= 0) return 0;
@@ -356,7 +400,7 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
     // the widest load class that A's rows (base + lda) and x all allow; the order of the
     // arithmetic does not depend on it (gemv.cuh)
     const uintptr_t al = reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.x);
-    int lw = ((al & 31) == 0 && a.lda % 8 == 0) ? 8 : ((al & 15) == 0 && a.lda % 4 == 0) ? 4 : 1;
+    int lw = cap_lw(((al & 31) == 0 && a.lda % 8 == 0) ? 8 : ((al & 15) == 0 && a.lda % 4 == 0) ? 4 : 1);
     if (a.n >= GEMV_LONG_N) {  // long rows: the stand-alone dot's order (gemv_long.cuh)
         // few rows cannot fill the GPU with one CTA each: split them over (row, chunk)
         // CTAs when the caller gave a workspace large enough
@@ -372,9 +416,16 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
         return lw == 8 ? gemv_long_go<8, false>(a, s)
              : lw == 4 ? gemv_long_go<4, false>(a, s) : gemv_long_go<1, false>(a, s);
     }
+    // G1 toLocal(x): rows of GXS_NMIN..GXS_NMAX columns that split evenly over their
+    // threads, aligned, and enough of them to amortise one x staging per resident CTA
+    // (gemv_xs.cuh)
+    const int gx = var(LIFT_VAR_GEMV_X);
+    if (lw >= 4 && gxs_shape_ok(a.n) && (gx == 2 || (gx == 0 && gxs_auto(a.m, a.n))))
+        return a.y_peers ? gxs_trl<true>(a, lw, s) : gxs_trl<false>(a, lw, s);
     // rows and/or x at arbitrary 4-byte alignment: realigned 256-bit loads (common.cuh);
     // 2 = rows only (x 32-byte aligned), 3 = rows and x
-    if (lw == 1 && LIFT_GEMV_REALIGN) lw = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 ? 2 : 3;
+    if (lw == 1 && LIFT_GEMV_REALIGN && !lw_capped())
+        lw = (reinterpret_cast<uintptr_t>(a.x) & 31) == 0 ? 2 : 3;
     return a.y_peers ? gemv_trl<true>(a, lw, s) : gemv_trl<false>(a, lw, s);
 }
 
@@ -403,6 +454,25 @@ const char* lift_status_string(lift_status s) {
 
 size_t lift_workspace_bytes(int64_t n) { return ws_bytes_for(n < 0 ? 0 : n); }
 
+lift_status lift_set_variant(lift_variant knob, int value) {
+    if ((int)knob < 0 || (int)knob >= LIFT_VAR_COUNT) return LIFT_ERR_INVALID_VALUE;
+    bool ok = false;
+    switch (knob) {
+        case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
+        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 2; break;
+        case LIFT_VAR_TREE: ok = value >= 0 && value <= 2; break;
+        default: break;
+    }
+    if (!ok) return LIFT_ERR_INVALID_VALUE;
+    g_var[knob].store(value);
+    return LIFT_OK;
+}
+
+int lift_get_variant(lift_variant knob) {
+    if ((int)knob < 0 || (int)knob >= LIFT_VAR_COUNT) return -1;
+    return var(knob);
+}
+
 lift_status lift_debug_set_grid_limit(int max_ctas) {
     if (max_ctas < 0) return LIFT_ERR_INVALID_VALUE;
     g_grid_limit.store(max_ctas);
@@ -416,7 +486,7 @@ lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_str
     if (misaligned4(x) || misaligned4(y)) return LIFT_ERR_INVALID_VALUE;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const uintptr_t ax = reinterpret_cast<uintptr_t>(x), ay = reinterpret_cast<uintptr_t>(y);
-    const int lw = align_class(ax - ay);      // relative phase of x and y
+    const int lw = cap_lw(align_class(ax - ay));  // relative phase of x and y
     const uintptr_t boundary = (uintptr_t)lw * 4;
     int64_t head = (int64_t)(((boundary - (ax % boundary)) % boundary) / 4);
     if (head > n) head = n;
