@@ -13,8 +13,9 @@
  *
  * General contract (every entry point):
  *  - Storage is fp32 (reading R1 in DESIGN.md: the paper's elements are 4 bytes,
- *    P:1077-1080).  All array pointers are DEVICE pointers of the current CUDA
- *    device, at least 4-byte aligned; wider alignment only enables wider loads and
+ *    P:1077-1080).  All array pointers are DEVICE pointers of the stream's device (the
+ *    current device for a NULL stream; the call switches to that device for its
+ *    duration), at least 4-byte aligned; wider alignment only enables wider loads and
  *    never changes a result bit.
  *  - Every compute call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
  *    default stream): it validates its arguments on the host, enqueues exactly one
@@ -131,8 +132,10 @@ lift_status lift_scal_asum(int64_t n, float alpha, const float* x, float* y, flo
  *   (system-scope release), waits for all p flags of its own buffer and folds the p
  *   partials pairwise in rank order: every rank gets the SAME fp32 bits, equal to
  *   lift_combine over the gathered *_partial results — with no separate collective.
- *   p in [1, 32]; epoch > 0 and strictly increasing per call on the same buffers (two
- *   banks alternate by epoch parity); all p ranks must make the matching call.  The
+ *   p in [1, 32]; epoch > 0 and EXACTLY previous + 1 per call on the same exchange
+ *   buffers (two banks alternate by epoch parity; a peer can be at most one call ahead,
+ *   so consecutive calls must land in different banks); all p ranks must make the
+ *   matching call with the same epoch.  The
  *   wait is bounded (~10 s): on timeout *result = NaN and *error (device int, may be
  *   NULL) is set to 1.  Workspace as for lift_asum. */
 #define LIFT_IPC_HANDLE_BYTES 64
@@ -159,7 +162,10 @@ lift_status lift_dot_allreduce(int64_t n, const float* x, const float* y, float*
  *   rank's flag into every exchange buffer (xpeers, as for lift_*_allreduce, including
  *   the same epoch rule) and waits for all p flags.  When the kernel ends, this rank's
  *   y holds every rank's rows — bit-identical to lift_gemv + an all-gather.  m >= 1 on
- *   every rank; y_out is implied (y_peers[rank] + row0). */
+ *   every rank; y_out is implied (y_peers[rank] + row0).  A peer one call ahead stores
+ *   its next rows while this rank may still read this call's y, so callers alternate two
+ *   y buffers by epoch parity (dist.PeerExchange does).  On a peer timeout the error word
+ *   is set and the missing rows are left unwritten. */
 lift_status lift_gemv_allgather(int64_t m, int64_t n, float alpha, const float* A, int64_t lda,
                                 const float* x, float beta, const float* y,
                                 float* const* y_peers, int64_t row0, void* const* xpeers,
@@ -224,14 +230,12 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
  *     LIFT_VAR_GEMV_X      gemv rows of 2048..24576 columns: 0 auto, 1 x read through L1 and
  *                          widened per use, 2 x staged once per CTA as fp64 in shared memory
  *                          (persistent CTAs, Cluster Launch Control stealing)
- *     LIFT_VAR_TREE        intra-warp tree of asum/dot/gemv: 0 auto (= 1), 1 shuffle
- *                          butterfly, 2 shared-memory tree (iterate(split-2 reduce) in local
- *                          memory, as the paper's Fig. 7a/7b) */
+ *   (The other Fig. 7 axes — shared-memory tree vs shuffle butterfly, TMA bulk loads, chunk
+ *   size — are compile-time variants searched by scripts/tune.py.) */
 typedef enum {
     LIFT_VAR_LOAD_WIDTH = 0,
     LIFT_VAR_GEMV_X = 1,
-    LIFT_VAR_TREE = 2,
-    LIFT_VAR_COUNT = 3
+    LIFT_VAR_COUNT = 2
 } lift_variant;
 lift_status lift_set_variant(lift_variant knob, int value);
 int lift_get_variant(lift_variant knob);

@@ -15,6 +15,7 @@ fallback: a CPU tensor is an error, and a missing liblift.so fails at import.
 """
 from __future__ import annotations
 
+import contextlib
 import os
 import threading
 
@@ -30,6 +31,17 @@ __all__ = ["scal", "asum", "dot", "gemv", "asum_partial", "dot_partial", "combin
 
 def _stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+_NULL_CTX = contextlib.nullcontext()
+
+
+def _on(device: torch.device):
+    """liblift launches on the CURRENT device (its SM count and occupancies too), so a call
+    on another device's tensors runs with that device made current for its duration."""
+    if device.index is None or device.index == torch.cuda.current_device():
+        return _NULL_CTX
+    return torch.cuda.device(device)
 
 
 def _vec(t: torch.Tensor, name: str) -> torch.Tensor:
@@ -109,7 +121,7 @@ def set_grid_limit(max_ctas: int) -> None:
 
 
 #: NEXT-4 runtime strategy knobs (lift.h lift_variant); every value gives the same bits.
-VARIANTS = {"load_width": 0, "gemv_x": 1, "tree": 2}
+VARIANTS = {"load_width": 0, "gemv_x": 1}
 
 
 def set_variant(knob: str, value: int) -> None:
@@ -125,8 +137,9 @@ def scal(alpha: float, x: torch.Tensor, out: torch.Tensor | None = None) -> torc
     """y = alpha * x (lift_scal).  ``out`` may be ``x`` itself (in place)."""
     x = _vec(x, "x")
     y = _out(out, x.numel(), torch.float32, x.device)
-    check(lib.lift_scal(x.numel(), float(alpha), x.data_ptr(), y.data_ptr(),
-                        _stream_handle(x.device)))
+    with _on(x.device):
+        check(lib.lift_scal(x.numel(), float(alpha), x.data_ptr(), y.data_ptr(),
+                            _stream_handle(x.device)))
     return y
 
 
@@ -136,8 +149,9 @@ def asum(x: torch.Tensor, out: torch.Tensor | None = None,
     x = _vec(x, "x")
     r = _out(out, 1, torch.float32, x.device)
     w = ws or _workspace(x.numel(), x.device)
-    check(lib.lift_asum(x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
-                        _stream_handle(x.device)))
+    with _on(x.device):
+        check(lib.lift_asum(x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                            _stream_handle(x.device)))
     return r
 
 
@@ -151,8 +165,9 @@ def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None,
         raise ValueError("x and y must be on the same device")
     r = _out(out, 1, torch.float32, x.device)
     w = ws or _workspace(x.numel(), x.device)
-    check(lib.lift_dot(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
-                       _stream_handle(x.device)))
+    with _on(x.device):
+        check(lib.lift_dot(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                           _stream_handle(x.device)))
     return r
 
 
@@ -164,8 +179,9 @@ def scal_asum(alpha: float, x: torch.Tensor, out: torch.Tensor | None = None,
     y = _out(out, x.numel(), torch.float32, x.device)
     r = _out(result, 1, torch.float32, x.device, "result")
     w = ws or _workspace(x.numel(), x.device)
-    check(lib.lift_scal_asum(x.numel(), float(alpha), x.data_ptr(), y.data_ptr(), r.data_ptr(),
-                             w.ptr, w.nbytes, _stream_handle(x.device)))
+    with _on(x.device):
+        check(lib.lift_scal_asum(x.numel(), float(alpha), x.data_ptr(), y.data_ptr(), r.data_ptr(),
+                                 w.ptr, w.nbytes, _stream_handle(x.device)))
     return y, r
 
 
@@ -175,8 +191,9 @@ def asum_partial(x: torch.Tensor, out: torch.Tensor | None = None,
     x = _vec(x, "x")
     r = _out(out, 1, torch.float64, x.device)
     w = ws or _workspace(x.numel(), x.device)
-    check(lib.lift_asum_partial(x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
-                                _stream_handle(x.device)))
+    with _on(x.device):
+        check(lib.lift_asum_partial(x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                                    _stream_handle(x.device)))
     return r
 
 
@@ -188,8 +205,9 @@ def dot_partial(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = Non
         raise ValueError("zip-length-mismatch: dot needs equal lengths (PAPER.md P:307)")
     r = _out(out, 1, torch.float64, x.device)
     w = ws or _workspace(x.numel(), x.device)
-    check(lib.lift_dot_partial(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr,
-                               w.nbytes, _stream_handle(x.device)))
+    with _on(x.device):
+        check(lib.lift_dot_partial(x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr,
+                                   w.nbytes, _stream_handle(x.device)))
     return r
 
 
@@ -200,8 +218,9 @@ def combine(partials: torch.Tensor, out: torch.Tensor | None = None) -> torch.Te
             and partials.numel() >= 1):
         raise ValueError("partials must be a non-empty contiguous float64 CUDA tensor")
     r = _out(out, 1, torch.float32, partials.device)
-    check(lib.lift_combine(partials.numel(), partials.data_ptr(), r.data_ptr(),
-                           _stream_handle(partials.device)))
+    with _on(partials.device):
+        check(lib.lift_combine(partials.numel(), partials.data_ptr(), r.data_ptr(),
+                               _stream_handle(partials.device)))
     return r
 
 
@@ -223,14 +242,15 @@ def gemv(A: torch.Tensor, x: torch.Tensor, y: torch.Tensor, alpha: float, beta: 
         raise ValueError(f"dimension-mismatch: A is {m}x{n}, x has {x.numel()}, "
                          f"y has {y.numel()}")
     yo = _out(out, m, torch.float32, A.device)
-    need = int(lib.lift_gemv_workspace_bytes(m, n)) if split else 0
-    wp, wb = (0, 0)
-    if need:  # rows >= 65536 columns: the split path needs a workspace (lift_gemv_ws)
-        w = _gemv_workspace(need, A.device)
-        wp, wb = w.data_ptr(), w.numel()
-    check(lib.lift_gemv_ws(m, n, float(alpha), A.data_ptr(), lda, x.data_ptr(), float(beta),
-                           y.data_ptr(), yo.data_ptr(), wp or None, wb,
-                           _stream_handle(A.device)))
+    with _on(A.device):
+        need = int(lib.lift_gemv_workspace_bytes(m, n)) if split else 0  # device's SM count
+        wp, wb = (0, 0)
+        if need:  # rows >= 65536 columns: the split path needs a workspace (lift_gemv_ws)
+            w = _gemv_workspace(need, A.device)
+            wp, wb = w.data_ptr(), w.numel()
+        check(lib.lift_gemv_ws(m, n, float(alpha), A.data_ptr(), lda, x.data_ptr(), float(beta),
+                               y.data_ptr(), yo.data_ptr(), wp or None, wb,
+                               _stream_handle(A.device)))
     return yo
 
 
@@ -254,6 +274,7 @@ def blackscholes(s: torch.Tensor, K: float, r: float, v: float, T: float,
     s = _vec(s, "s")
     c = _out(call, s.numel(), torch.float32, s.device, "call")
     p = _out(put, s.numel(), torch.float32, s.device, "put")
-    check(lib.lift_blackscholes(s.numel(), s.data_ptr(), float(K), float(r), float(v), float(T),
-                                c.data_ptr(), p.data_ptr(), _stream_handle(s.device)))
+    with _on(s.device):
+        check(lib.lift_blackscholes(s.numel(), s.data_ptr(), float(K), float(r), float(v), float(T),
+                                    c.data_ptr(), p.data_ptr(), _stream_handle(s.device)))
     return c, p

@@ -460,7 +460,6 @@ lift_status lift_set_variant(lift_variant knob, int value) {
     switch (knob) {
         case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
         case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 2; break;
-        case LIFT_VAR_TREE: ok = value >= 0 && value <= 2; break;
         default: break;
     }
     if (!ok) return LIFT_ERR_INVALID_VALUE;

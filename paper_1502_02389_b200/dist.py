@@ -170,10 +170,11 @@ class PeerExchange:
         x = lift._vec(x_shard, "x")
         r = lift._out(out, 1, torch.float32, x.device)
         w = ws or lift._workspace(x.numel(), x.device)
-        self.epoch += 1
-        self._check(self._lib.lift_asum_allreduce(
-            x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes, self.peers.data_ptr(),
-            self.p, self.rank, self.epoch, self.error.data_ptr(), self._stream()))
+        self.epoch += 1  # the ABI needs epoch = previous + 1 per exchange buffer (bank parity)
+        with torch.cuda.device(self.device):
+            self._check(self._lib.lift_asum_allreduce(
+                x.numel(), x.data_ptr(), r.data_ptr(), w.ptr, w.nbytes, self.peers.data_ptr(),
+                self.p, self.rank, self.epoch, self.error.data_ptr(), self._stream()))
         return r
 
     def dot(self, x_shard, y_shard, out=None, ws=None):
@@ -184,10 +185,11 @@ class PeerExchange:
         r = lift._out(out, 1, torch.float32, x.device)
         w = ws or lift._workspace(x.numel(), x.device)
         self.epoch += 1
-        self._check(self._lib.lift_dot_allreduce(
-            x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
-            self.peers.data_ptr(), self.p, self.rank, self.epoch, self.error.data_ptr(),
-            self._stream()))
+        with torch.cuda.device(self.device):
+            self._check(self._lib.lift_dot_allreduce(
+                x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(), w.ptr, w.nbytes,
+                self.peers.data_ptr(), self.p, self.rank, self.epoch, self.error.data_ptr(),
+                self._stream()))
         return r
 
     def _share(self, own_ptr):
@@ -212,15 +214,20 @@ class PeerExchange:
         return ptrs, opened
 
     def _full_y(self, m: int):
+        """Two banks (epoch parity) of a full-length y per rank, IPC-shared: a peer can be at
+        most one call ahead (finishing call e needs every rank's call-e rows), so it writes
+        call e+1's rows into the other bank while this rank may still read call e's."""
         if self._y is not None and self._y[0] == m:
             return self._y
         self._free_y()
         buf = ctypes.c_void_p()
-        self._check(self._lib.lift_ipc_alloc(max(4, 4 * m), ctypes.byref(buf)))
+        self._check(self._lib.lift_ipc_alloc(max(8, 8 * m), ctypes.byref(buf)))
         ptrs, opened = self._share(buf.value)
-        arr = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
-        view = torch.as_tensor(_DevArray(buf.value, m, self.device.index), device=self.device)
-        self._y = (m, buf.value, opened, arr, view)
+        arrs = [torch.tensor([p + 4 * m * b for p in ptrs], dtype=torch.int64, device=self.device)
+                for b in (0, 1)]
+        base = torch.as_tensor(_DevArray(buf.value, 2 * m, self.device.index), device=self.device)
+        views = [base[:m], base[m:]]
+        self._y = (m, buf.value, opened, arrs, views)
         return self._y
 
     def _free_y(self):
@@ -236,29 +243,47 @@ class PeerExchange:
 
     def gemv(self, A_rows, x, y_rows, alpha: float, beta: float, m: int, row0: int):
         """y_full = alpha*A@x + beta*y over all ranks' rows, the all-gather fused into the
-        gemv kernel (lift_gemv_allgather).  Returns this rank's full-length y (a view of
-        the IPC-shared buffer; valid until the next call with another m or close())."""
+        gemv kernel (lift_gemv_allgather).  Returns this rank's full-length y: a view of
+        the IPC-shared bank of this call (banks alternate by call).  It stays valid until
+        this rank's next-but-one call; work enqueued on this stream before the next call
+        may read it.  Every rank must own >= 1 row (m >= world)."""
         lift = _lift()
         if not (A_rows.is_cuda and A_rows.dtype == torch.float32 and A_rows.dim() == 2):
             raise ValueError("A must be a 2-D float32 CUDA tensor")
         ml, n = A_rows.shape
         if ml > 0 and n > 0 and A_rows.stride(1) != 1:
             raise ValueError("A must be row-major with unit column stride")
+        if m < self.p:
+            raise ValueError(f"fused all-gather needs m >= world ({m} < {self.p}): every rank "
+                             "must own at least one row")
         lda = A_rows.stride(0) if (ml > 1 and n > 0) else max(1, n)
         x, y = lift._vec(x, "x"), lift._vec(y_rows, "y")
         if x.numel() != n or y.numel() != ml:
             raise ValueError("dimension-mismatch")
-        _, _, _, arr, view = self._full_y(m)
+        if ml == 0:
+            raise ValueError("this rank owns no rows (use row_range)")
+        _, _, _, arrs, views = self._full_y(m)
         self.epoch += 1
-        self._check(self._lib.lift_gemv_allgather(
-            ml, n, float(alpha), A_rows.data_ptr(), lda, x.data_ptr(), float(beta), y.data_ptr(),
-            arr.data_ptr(), row0, self.peers.data_ptr(), self.p, self.rank, self.epoch,
-            self.error.data_ptr(), self._stream()))
-        return view
+        bank = self.epoch & 1
+        with torch.cuda.device(self.device):
+            self._check(self._lib.lift_gemv_allgather(
+                ml, n, float(alpha), A_rows.data_ptr(), lda, x.data_ptr(), float(beta),
+                y.data_ptr(), arrs[bank].data_ptr(), row0, self.peers.data_ptr(), self.p,
+                self.rank, self.epoch, self.error.data_ptr(), self._stream()))
+        return views[bank]
+
+    def check(self):
+        """Raise if any exchange of this object timed out (a peer missed an epoch): the
+        kernel then returned NaN (asum/dot) or an incomplete y (gemv) and set the error
+        word.  Synchronises this device."""
+        if int(self.error.item()) != 0:
+            raise RuntimeError("PeerExchange: a peer did not arrive within the bounded wait "
+                               "(~10 s); results of the affected calls are invalid")
 
     def close(self):
         self._free_y()
         torch.cuda.synchronize(self.device)
+        err = int(self.error.item()) if self.error is not None else 0
         if self.p > 1 and dist.is_initialized():
             dist.barrier(group=self.group)  # nobody still writes into our buffer
         for ptr in self.opened:
@@ -267,6 +292,9 @@ class PeerExchange:
         if self.buf:
             self._lib.lift_xchg_destroy(self.buf)
             self.buf = None
+        if err:
+            raise RuntimeError("PeerExchange: a peer exchange timed out during this object's "
+                               "lifetime; see check()")
 
 
 class _DevArray:

@@ -178,3 +178,15 @@ def test_c_example_runs(tmp_path):
     assert _build_c_example(exe).returncode == 0
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_variant_api_host_only():
+    """NEXT-4 knobs: valid values round-trip, bad knobs/values are rejected (no GPU needed)."""
+    from paper_1502_02389_b200._lib import lib
+    assert lib.lift_set_variant(0, 3) == INVALID   # load width 3
+    assert lib.lift_set_variant(1, 7) == INVALID   # gemv x strategy 7
+    assert lib.lift_set_variant(9, 0) == INVALID   # no such knob
+    assert lib.lift_get_variant(9) == -1
+    for knob, v in ((0, 4), (0, 1), (1, 2)):
+        assert lib.lift_set_variant(knob, v) == OK and lib.lift_get_variant(knob) == v
+        assert lib.lift_set_variant(knob, 0) == OK and lib.lift_get_variant(knob) == 0

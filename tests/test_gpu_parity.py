@@ -2,11 +2,11 @@
 
 Bars (BASELINE.json north_star):
   * scal: bit-exact RN(alpha*x_i) at every size, alignment and aliasing;
-  * asum/dot: relative error <= 1e-5 (condition-scaled, |g-o| <= 1e-5*sum|terms|,
-    for signed dot inputs); bit-exact on integer-valued inputs, where the sum is
-    unique; bit-identical run to run and across grid sizes;
-  * gemv: per element relative error <= 1e-6 (condition-scaled for signed inputs);
-    identity matrix bit-exact.
+  * asum/dot: relative error |g-o| <= 1e-5 |o| (plain relative, also for
+    signed inputs); bit-exact on integer-valued inputs, where the sum is unique;
+    bit-identical run to run and across grid sizes;
+  * gemv: per element relative error |g-o| <= 1e-6 |o| (plain relative, also for signed
+    inputs); identity matrix bit-exact.
 """
 import numpy as np
 import pytest
@@ -116,9 +116,9 @@ def test_asum_dot_tolerance(lift, n):
     d = float(lift.dot(dev(xp), dev(y)).item())
     do = oracle.dot(xp, y)
     assert abs(d - do) <= 1e-5 * abs(do)
-    ds = float(lift.dot(dev(x), dev(y)).item())  # signed: condition-scaled
+    ds = float(lift.dot(dev(x), dev(y)).item())  # signed: plain relative too (A20)
     dso = oracle.dot(x, y)
-    assert abs(ds - dso) <= 1e-5 * oracle.dot(np.abs(x), y)
+    assert abs(ds - dso) <= 1e-5 * abs(dso), (ds, dso)
 
 
 @pytest.mark.parametrize("n", [1, 9, 1000, RED_C + 1, 5 * RED_C + 3, GROUP + 1, 1 << 20])
@@ -268,11 +268,15 @@ def gemv_inputs(m, n, seed, signed=False):
 
 
 def check_gemv(got, A, x, y, alpha, beta):
+    """Plain relative error per element; the condition-scaled error
+    |g-o| / sum|terms| is reported as a diagnostic only."""
     ref = oracle.gemv(A, x, y, alpha, beta)
     scale = abs(alpha) * (np.abs(A.astype(np.float64)) @ np.abs(x.astype(np.float64))) \
         + abs(beta) * np.abs(y.astype(np.float64))
     err = np.abs(got.astype(np.float64) - ref)
-    assert np.all(err <= 1e-6 * scale), float(np.max(err / np.maximum(scale, 1e-300)))
+    assert np.all(err <= 1e-6 * np.abs(ref)), (
+        float(np.max(err / np.maximum(np.abs(ref), 1e-300))),
+        float(np.max(err / np.maximum(scale, 1e-300))))
     return ref
 
 
@@ -285,8 +289,8 @@ def test_gemv_tolerance(lift, m, n):
     assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref))
 
 
-@pytest.mark.parametrize("m,n", [(37, 1029), (8, 20000)])
-def test_gemv_signed_condition_scaled(lift, m, n):
+@pytest.mark.parametrize("m,n", [(37, 1029), (8, 20000), (1000, 8192), (64, 70000)])
+def test_gemv_signed_plain_relative(lift, m, n):
     A, x, y = gemv_inputs(m, n, 5, signed=True)
     got = lift.gemv(dev(A), dev(x), dev(y), -2.0, 0.75).cpu().numpy()
     check_gemv(got, A, x, y, -2.0, 0.75)
@@ -354,15 +358,17 @@ def dev_gen(n, seed, tid, lo=-1.0, hi=1.0, dist=0):
     return gen.fill_device(t, seed, tid, 0, dist, lo, hi)
 
 
-def test_full_scal_2p28_sampled(lift):
+def test_full_scal_2p28_every_element(lift):
+    """All 2^28 outputs compared bitwise with the oracle (in 2^24-element blocks)."""
     n = 1 << 28
     x = dev_gen(n, 0, gen.TID_X)
     y = lift.scal(3.0, x)
-    idx = torch.tensor(np.r_[0:1000, n - 1000:n,
-                             np.random.default_rng(0).integers(0, n, 100_000)], device=DEV)
-    xs = x[idx].cpu().numpy()
-    assert np.array_equal(bits(y[idx]), oracle.scal(3.0, xs).astype(np.float32).view(np.uint32))
+    xh, yh = x.cpu().numpy(), y.cpu().numpy()
     del x, y
+    B = 1 << 24
+    for i in range(0, n, B):
+        ref = oracle.scal(3.0, xh[i:i + B]).astype(np.float32)
+        assert np.array_equal(yh[i:i + B].view(np.uint32), ref.view(np.uint32)), i
 
 
 def test_full_asum_2p28(lift):

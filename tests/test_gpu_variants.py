@@ -1,0 +1,72 @@
+"""NEXT-4 runtime strategy variants (lift_set_variant): every value of every knob computes the
+SAME canonical order, so results must be bit-identical to the default (and hence to the
+oracle-checked default path).  Shapes cover the vector bodies, scalar heads/tails, the
+reduction's partial chunks and the gemv paths the knobs switch between."""
+import numpy as np
+import pytest
+import torch
+
+import lift_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture
+def lift():
+    import paper_1502_02389_b200 as m
+    yield m
+    for k in m.VARIANTS:
+        m.set_variant(k, 0)
+
+
+def bits(t):
+    return t.detach().cpu().numpy().view(np.uint32).copy()
+
+
+def fill(n, seed, tid, lo=-1.0, hi=1.0, off=0):
+    buf = torch.empty(n + off, dtype=torch.float32, device=DEV)
+    v = buf[off:]
+    return gen.fill_device(v, seed, tid, 0, gen.DIST_UNIFORM, lo, hi)
+
+
+def run_all(lift, off):
+    out = []
+    for n in (1, 9, 8191, 8192 * 3 + 5, 1 << 20):
+        x = fill(n, 1, gen.TID_X, off=off)
+        y = fill(n, 1, gen.TID_Y, off=off)
+        out += [bits(lift.scal(3.0, x)), bits(lift.asum(x)), bits(lift.dot(x, y))]
+    for m, n in ((300, 2048), (257, 4096), (64, 8192), (33, 16384), (16, 24576), (7, 1000)):
+        A = fill(m * n, 2, gen.TID_A, 0.0, 3.0).view(m, n)
+        gx = fill(n, 2, gen.TID_X, 0.0, 1.0)
+        gy = fill(m, 2, gen.TID_Y, 0.0, 2.0)
+        out.append(bits(lift.gemv(A, gx, gy, 1.5, 0.5)))
+    return out
+
+
+@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2))])
+@pytest.mark.parametrize("off", [0, 4])
+def test_variants_bit_identical(lift, knob, values, off):
+    ref = run_all(lift, off)
+    for v in values:
+        lift.set_variant(knob, v)
+        assert lift.get_variant(knob) == v
+        got = run_all(lift, off)
+        for i, (a, b) in enumerate(zip(ref, got)):
+            assert np.array_equal(a, b), (knob, v, i)
+        lift.set_variant(knob, 0)
+
+
+def test_staged_x_gemv_matches_oracle(lift):
+    """The staged-x kernel (LIFT_VAR_GEMV_X = 2) against the oracle directly, with a partial
+    last row block and signed inputs."""
+    lift.set_variant("gemv_x", 2)
+    for m, n in ((1001, 8192), (65, 4096), (3, 16384)):
+        A = gen.host(m * n, 7, gen.TID_A).reshape(m, n)
+        x = gen.host(n, 7, gen.TID_X)
+        y = gen.host(m, 7, gen.TID_Y)
+        got = lift.gemv(torch.from_numpy(A).to(DEV), torch.from_numpy(x).to(DEV),
+                        torch.from_numpy(y).to(DEV), -1.25, 0.75).cpu().numpy().astype(np.float64)
+        ref = oracle.gemv(A, x, y, -1.25, 0.75)
+        assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (m, n)

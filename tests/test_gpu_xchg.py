@@ -106,6 +106,22 @@ def test_fused_exchange_two_processes_one_gpu():
         full = lift.gemv(A, gx, gy, 1.5, 0.5).cpu().numpy().view(np.uint32).tolist()
         assert res[0][6 + j] == full and res[1][6 + j] == full
     assert res[0][9] == 0 and res[1][9] == 0     # no timeouts
+    # against the ORACLE (not only other CUDA calls): asum/dot <= 1e-5, gemv <= 1e-6
+    import oracle
+    for it, groups in enumerate([8, 8, 2, 1, 8]):
+        n = groups * lift.GROUP_ELEMS + (0 if it != 4 else 12345)
+        xh = gen.host(n, it, gen.TID_X)
+        yh = gen.host(n, it, gen.TID_Y)
+        ra = float(np.array(res[0][it][0], np.uint32).view(np.float32)[0])
+        rd = float(np.array(res[0][it][1], np.uint32).view(np.float32)[0])
+        ao, do = oracle.asum(xh), oracle.dot(xh, yh)
+        assert abs(ra - ao) <= 1e-5 * abs(ao), (it, ra, ao)
+        assert abs(rd - do) <= 1e-5 * abs(do), (it, rd, do)
+    for j, (m, k) in enumerate([(1001, 777), (300, 8192), (5, 70003)]):
+        A = gen.host(m * k, 4, gen.TID_A).reshape(m, k)
+        ref = oracle.gemv(A, gen.host(k, 4, gen.TID_X), gen.host(m, 4, gen.TID_Y), 1.5, 0.5)
+        got = np.array(res[0][6 + j], np.uint32).view(np.float32).astype(np.float64)
+        assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), j
 
 
 def test_fused_exchange_single_rank():
