@@ -78,6 +78,9 @@ int lift_reduce_group_chunks(void);
 
 /* Static, NUL-terminated description of a status code. */
 const char* lift_status_string(lift_status s);
+/* The CUDA error behind the calling thread's last LIFT_ERR_CUDA (cudaGetErrorString), or
+ * "no error".  Static string; host only. */
+const char* lift_last_cuda_error(void);
 
 /* Bytes of workspace lift_asum / lift_dot / *_partial need for length n (a multiple of
  * 16).  The workspace holds the single-pass reduction's chunk/group partials (from its

@@ -20,7 +20,7 @@ EXPORTS = (
     "lift_xchg_create", "lift_xchg_destroy", "lift_ipc_get_handle", "lift_ipc_open_handle",
     "lift_ipc_close_handle", "lift_asum_allreduce", "lift_dot_allreduce", "lift_ipc_alloc",
     "lift_gemv_allgather", "lift_gemv_ws", "lift_gemv_workspace_bytes", "lift_set_variant",
-    "lift_get_variant",
+    "lift_get_variant", "lift_last_cuda_error",
 )
 
 LIFT_OK = 0
@@ -51,6 +51,7 @@ def _load():
         "lift_gemv_workspace_bytes": ([_i64, _i64], _sz),
         "lift_set_variant": ([_int, _int], _int),
         "lift_get_variant": ([_int], _int),
+        "lift_last_cuda_error": ([], ctypes.c_char_p),
         "lift_debug_set_grid_limit": ([_int], _int),
         "lift_reduce_chunk_elems": ([], _i64),
         "lift_reduce_group_chunks": ([], _int),
@@ -88,4 +89,7 @@ class LiftError(RuntimeError):
 
 def check(status: int) -> None:
     if status != LIFT_OK:
-        raise LiftError(lib.lift_status_string(status).decode())
+        msg = lib.lift_status_string(status).decode()
+        if status == 4:  # LIFT_ERR_CUDA: name the CUDA error behind it
+            msg += f" ({lib.lift_last_cuda_error().decode()})"
+        raise LiftError(msg)

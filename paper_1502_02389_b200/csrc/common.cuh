@@ -91,10 +91,37 @@ __device__ __forceinline__ double pairwise8(const double* v) {
 // Warp butterfly with xor distances 1,2,4,8,16: a pairwise tree over lanes in
 // ascending adjacent pairs (IEEE addition is commutative, so lanes i and i^d get
 // bit-identical sums).  Every lane ends with the warp total.
+//
+// NEXT-4 tree axis (compile-time, scripts/tune.py): LIFT_TREE = 2 builds the same tree as
+// the paper's Fig. 7a/7b lowering, toLocal + iterate^5(split-2 reduce) in shared memory
+// with a warp barrier per level: level s keeps b[i] = b[2i] + b[2i+1] for i < s — the
+// same adjacent pairs, so the same bits as the butterfly.
+#ifndef LIFT_TREE
+#define LIFT_TREE 1  // 1: shuffle butterfly, 2: shared-memory tree
+#endif
 __device__ __forceinline__ double warp_pairwise(double v) {
+#if LIFT_TREE == 2
+    __shared__ double tree_buf[32][32];  // one row per warp of the CTA (<= 1024 threads)
+    const int lane = threadIdx.x & 31;
+    double* b = tree_buf[threadIdx.x >> 5];
+    b[lane] = v;
+    __syncwarp();
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        double t = 0.0;
+        if (lane < s) t = __dadd_rn(b[2 * lane], b[2 * lane + 1]);
+        __syncwarp();
+        if (lane < s) b[lane] = t;
+        __syncwarp();
+    }
+    const double r = b[0];
+    __syncwarp();
+    return r;
+#else
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, d));
     return v;
+#endif
 }
 
 // LW == 2 (gemv rows, asum/dot operands): data at any 4-byte alignment (odd n with
@@ -191,6 +218,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
     }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// TMA bulk copies (cp.async.bulk -> SASS UBLKCP): global -> shared completes `bar` by
+// transaction bytes; shared -> global is tracked by the issuing thread's bulk groups.
+// Addresses and sizes must be multiples of 16 bytes.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src_smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 struct Clc {

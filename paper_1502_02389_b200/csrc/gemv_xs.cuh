@@ -79,7 +79,7 @@ __device__ __forceinline__ void gxs_fold(const f8& av, const double2* xs, int64_
 
 template <int TRL, int LW, bool PEERS>
 __global__ void __launch_bounds__(GXS_T, LIFT_GXS_MINB) gemv_xs_kernel(GemvArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* clc_bar = reinterpret_cast<uint64_t*>(smem);
     uint4* clc_resp = reinterpret_cast<uint4*>(smem + 16);
     double(*wv)[GXS_T / 32] = reinterpret_cast<double(*)[GXS_T / 32]>(smem + 64);

@@ -15,6 +15,7 @@
 #include "blackscholes.cuh"
 #include "gemv.cuh"
 #include "gemv_xs.cuh"
+#include "gemv_tma.cuh"
 #include "reduce.cuh"
 #include "gemv_long.cuh"
 #include "scal.cuh"
@@ -103,11 +104,14 @@ int occupancy(const void* fn, int threads, size_t smem) {
             return g_occ[i].blocks;
     // The attribute is a per-function maximum: set it to the device's opt-in maximum, so
     // launches with any dynamic smem size (other n) stay valid whatever the call order.
-    if (smem > 48 * 1024) {
+    if (smem > 48 * 1024) {  // the opt-in maximum minus the kernel's static shared memory
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, fn);
+        const int room = optin - (int)fa.sharedSizeBytes;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             optin > (int)smem ? optin : (int)smem);
+                             room > (int)smem ? room : (int)smem);
     }
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, threads, smem) != cudaSuccess ||
@@ -159,8 +163,13 @@ void launch(void (*k)(KArgs...), int64_t grid, int block, size_t smem, cudaStrea
     cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+thread_local cudaError_t g_last_cuda = cudaSuccess;  // the last failed launch of this thread
+
 lift_status launched() {
-    return cudaGetLastError() == cudaSuccess ? LIFT_OK : LIFT_ERR_CUDA;
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) return LIFT_OK;
+    g_last_cuda = e;
+    return LIFT_ERR_CUDA;
 }
 
 // Workspace layout for a buffer of W bytes (W floored to 16):
@@ -272,9 +281,12 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
                    : lw == 2 ? (const void*)reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>
                              : (const void*)reduce_kernel<Op, 1, B>;
-    const int64_t grid = grid_for(L.nc, fn, RED_T, 0, LIFT_PERSISTENT);
-    if (lw == 8) launch(reduce_kernel<Op, 8, B>, grid, RED_T, 0, stream, a);
-    else if (lw == 4) launch(reduce_kernel<Op, 4, B>, grid, RED_T, 0, stream, a);
+    // NEXT-4 TMA variant: the chunk buffers are dynamic shared memory
+    const size_t tsm = (LIFT_RED_TMA && lw >= 4 && !Op::kMapStore)
+                           ? (size_t)RED_C * 4 * (Op::kTwoInputs ? 2 : 1) : 0;
+    const int64_t grid = grid_for(L.nc, fn, RED_T, tsm, LIFT_PERSISTENT);
+    if (lw == 8) launch(reduce_kernel<Op, 8, B>, grid, RED_T, tsm, stream, a);
+    else if (lw == 4) launch(reduce_kernel<Op, 4, B>, grid, RED_T, tsm, stream, a);
     else if (lw == 2) launch(reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>, grid, RED_T, 0, stream, a);
     else launch(reduce_kernel<Op, 1, B>, grid, RED_T, 0, stream, a);
     return launched();
@@ -349,6 +361,33 @@ lift_status gxs_go(GemvArgs a, cudaStream_t s) {
     return launched();
 }
 
+template <int TRL, bool PEERS>
+lift_status gtm_go(GemvArgs a, int nst, cudaStream_t s) {
+    constexpr int64_t rb = (GTM_CT >> TRL) * GTM_R;  // rows per block
+    a.nblocks = (a.m + rb - 1) / rb;
+    const size_t smem = gtm_smem_bytes(a.n, nst);
+    const void* fn = (const void*)gemv_tma_kernel<TRL, PEERS>;
+    const int64_t grid = grid_for(a.nblocks, fn, GTM_T, smem, false, true);
+    launch(gemv_tma_kernel<TRL, PEERS>, grid, GTM_T, smem, s, a, nst);
+    return launched();
+}
+
+template <bool PEERS>
+lift_status gtm_trl(const GemvArgs& a, int nst, cudaStream_t s) {
+    switch (gemv_tr_log2(a.n)) {  // n >= 2048: 32..256 threads per row
+        case 8: return gtm_go<8, PEERS>(a, nst, s);
+        case 7: return gtm_go<7, PEERS>(a, nst, s);
+        case 6: return gtm_go<6, PEERS>(a, nst, s);
+        default: return gtm_go<5, PEERS>(a, nst, s);
+    }
+}
+
+int smem_optin(int dev) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
 template <bool PEERS>
 lift_status gxs_trl(const GemvArgs& a, int lw, cudaStream_t s) {
     switch (gemv_tr_log2(a.n)) {  // n >= GXS_NMIN: 32..256 threads per row
@@ -420,6 +459,10 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
     // threads, aligned, and enough of them to amortise one x staging per resident CTA
     // (gemv_xs.cuh)
     const int gx = var(LIFT_VAR_GEMV_X);
+    if (gx == 3 && lw >= 4 && gtm_shape_ok(a.n)) {  // TMA ring (gemv_tma.cuh)
+        const int nst = gtm_stages(a.n, (size_t)smem_optin(current_device()));
+        if (nst >= 2) return a.y_peers ? gtm_trl<true>(a, nst, s) : gtm_trl<false>(a, nst, s);
+    }
     if (lw >= 4 && gxs_shape_ok(a.n) && (gx == 2 || (gx == 0 && gxs_auto(a.m, a.n))))
         return a.y_peers ? gxs_trl<true>(a, lw, s) : gxs_trl<false>(a, lw, s);
     // rows and/or x at arbitrary 4-byte alignment: realigned 256-bit loads (common.cuh);
@@ -452,6 +495,10 @@ const char* lift_status_string(lift_status s) {
     return "LIFT_ERR_UNKNOWN";
 }
 
+const char* lift_last_cuda_error(void) {
+    return g_last_cuda == cudaSuccess ? "no error" : cudaGetErrorString(g_last_cuda);
+}
+
 size_t lift_workspace_bytes(int64_t n) { return ws_bytes_for(n < 0 ? 0 : n); }
 
 lift_status lift_set_variant(lift_variant knob, int value) {
@@ -459,7 +506,7 @@ lift_status lift_set_variant(lift_variant knob, int value) {
     bool ok = false;
     switch (knob) {
         case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
-        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 2; break;
+        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 3; break;
         default: break;
     }
     if (!ok) return LIFT_ERR_INVALID_VALUE;
@@ -494,6 +541,12 @@ lift_status lift_scal(int64_t n, float alpha, const float* x, float* y, lift_str
     const int tail = (int)(body % 8);
     const bool alias = (x == y);
     const void* fn = lw == 8 ? scal_fn<8>(alias) : lw == 4 ? scal_fn<4>(alias) : scal_fn<1>(alias);
+    if (LIFT_SCAL_TMA && lw >= 4) {  // NEXT-4 TMA bulk variant (compile-time)
+        const int64_t tiles = (8 * nslots + SCAL_TMA_TILE - 1) / SCAL_TMA_TILE;
+        const int64_t grid = grid_for(tiles, (const void*)scal_tma_kernel, SCAL_TMA_T, 0, false);
+        launch(scal_tma_kernel, grid, SCAL_TMA_T, 0, s, nslots, (int)head, tail, alpha, x, y);
+        return launched();
+    }
     const int64_t tile = (int64_t)SCAL_T * SCAL_U;
     const int64_t grid = grid_for((nslots + tile - 1) / tile, fn, SCAL_T, LIFT_SCAL_SMEM, LIFT_PERSISTENT);
     if (lw == 8) alias ? scal_go<8, true>(grid, nslots, (int)head, tail, alpha, x, y, s)

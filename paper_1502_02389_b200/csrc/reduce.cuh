@@ -45,6 +45,12 @@ namespace lift {
 #ifndef LIFT_RED_RB
 #define LIFT_RED_RB 2
 #endif
+#ifndef LIFT_RED_TMA
+#define LIFT_RED_TMA 0  // NEXT-4 (tune.py): chunks arrive by TMA bulk copy into shared memory
+#endif
+#ifndef LIFT_RED_TMA
+#define LIFT_RED_TMA 0  // NEXT-4 (tune.py): chunks arrive by TMA bulk copy into shared memory
+#endif
 #ifndef LIFT_SC_FENCE
 #define LIFT_SC_FENCE 0
 #endif
@@ -283,6 +289,43 @@ __device__ __forceinline__ void chunk_body_full(const float* xc, const float* yc
     }
 }
 
+// NEXT-4 load axis, TMA bulk variant (compile-time LIFT_RED_TMA = 1; scripts/tune.py): the
+// chunk's x (and y) arrive in shared memory by one bulk copy each (an mbarrier completes by
+// bytes); lanes then read their vectors t + 256k from shared memory — the same values in
+// the same order, so the same bits.  Full, 16-byte-aligned chunks only.
+template <class Op>
+__device__ __forceinline__ void chunk_body_tma(const float* xc, const float* yc,
+                                               typename Op::acc_t* acc, uint64_t* bar,
+                                               uint32_t& phase) {
+    extern __shared__ __align__(128) unsigned char red_smem[];
+    float* xs = reinterpret_cast<float*>(red_smem);
+    float* ys = xs + RED_C;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        mbar_arrive_expect_tx(bar, (uint32_t)(RED_C * 4 * (Op::kTwoInputs ? 2 : 1)));
+        bulk_g2s(xs, xc, RED_C * 4, bar);
+        if constexpr (Op::kTwoInputs) bulk_g2s(ys, yc, RED_C * 4, bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+#pragma unroll
+    for (int k = 0; k < RED_K; ++k) {
+        const int q = t + k * RED_T;
+        const float4 a0 = reinterpret_cast<const float4*>(xs)[2 * q];
+        const float4 a1 = reinterpret_cast<const float4*>(xs)[2 * q + 1];
+        const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        float yv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if constexpr (Op::kTwoInputs) {
+            const float4 b0 = reinterpret_cast<const float4*>(ys)[2 * q];
+            const float4 b1 = reinterpret_cast<const float4*>(ys)[2 * q + 1];
+            yv[0] = b0.x; yv[1] = b0.y; yv[2] = b0.z; yv[3] = b0.w;
+            yv[4] = b1.x; yv[5] = b1.y; yv[6] = b1.z; yv[7] = b1.w;
+        }
+#pragma unroll
+        for (int e = 0; e < RED_V; ++e) acc[e] = Op::step(acc[e], xv[e], yv[e]);
+    }
+}
+
 // Partial last chunk: same order, elements >= n skipped.  Skipping equals adding
 // +0 exactly (the accumulators start at +0 and can never become -0 in RN).
 template <class Op>
@@ -437,6 +480,13 @@ __global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBloc
     pdl_wait();
     pdl_trigger();
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
+    constexpr bool kTma = LIFT_RED_TMA && LW >= 4 && !Op::kMapStore;
+    __shared__ uint64_t tma_bar;
+    uint32_t tma_phase = 0;
+    if constexpr (kTma) {
+        if (threadIdx.x == 0) mbar_init(&tma_bar, 1);
+        __syncthreads();
+    }
     int parity = 0;
     for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x, parity ^= 1) {
         trace_start(c);
@@ -448,7 +498,8 @@ __global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBloc
 #pragma unroll
         for (int e = 0; e < RED_V; ++e) acc[e] = 0;
         float* mo = Op::kMapStore ? a.map_out + base : nullptr;
-        if (base + RED_C <= a.n) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo, base, a.n);
+        if (kTma && base + RED_C <= a.n) chunk_body_tma<Op>(xc, yc, acc, &tma_bar, tma_phase);
+        else if (base + RED_C <= a.n) chunk_body_full<Op, LW, B>(xc, yc, acc, a.alpha, mo, base, a.n);
         else chunk_body_tail<Op>(xc, yc, a.n - base, acc, a.alpha, mo);
         chunk_finish<Op, LW, B>(a, c, acc, wbuf, parity);
     }

@@ -83,4 +83,59 @@ __global__ void __launch_bounds__(SCAL_T) scal_kernel(int64_t nslots, int head, 
     }
 }
 
+// NEXT-4 load axis, TMA bulk variant (compile-time LIFT_SCAL_TMA = 1; scripts/tune.py):
+// per tile the TMA engine copies SCAL_TMA_TILE floats of x into shared memory (one
+// mbarrier completes by bytes), the CTA scales them in place, and one bulk store writes the
+// tile to y.  Same RN(alpha * x_i) per element, so the same bits.  Needs x and y 16-byte
+// aligned after the head (the launcher's 128-/256-bit classes).
+#ifndef LIFT_SCAL_TMA
+#define LIFT_SCAL_TMA 0
+#endif
+constexpr int SCAL_TMA_T = 256;
+constexpr int SCAL_TMA_TILE = 8192;  // floats (32 KiB) per tile
+
+__global__ void __launch_bounds__(SCAL_TMA_T) scal_tma_kernel(int64_t nslots, int head, int tail,
+                                                               float alpha, const float* x, float* y) {
+    __shared__ __align__(128) float buf[SCAL_TMA_TILE];
+    __shared__ __align__(8) uint64_t bar;
+    pdl_wait();
+    pdl_trigger();
+    const int t = threadIdx.x;
+    if (t == 0) mbar_init(&bar, 1);
+    if (blockIdx.x == 0) {
+        if (t < head) y[t] = alpha * x[t];
+        const int64_t tb = head + 8 * nslots;
+        if (t >= 32 && t < 32 + tail) y[tb + (t - 32)] = alpha * x[tb + (t - 32)];
+    }
+    __syncthreads();
+    const float* xb = x + head;
+    float* yb = y + head;
+    const int64_t nf = 8 * nslots;
+    uint32_t phase = 0;
+    for (int64_t f0 = (int64_t)blockIdx.x * SCAL_TMA_TILE; f0 < nf;
+         f0 += (int64_t)gridDim.x * SCAL_TMA_TILE, phase ^= 1u) {
+        const int len = (int)(nf - f0 < SCAL_TMA_TILE ? nf - f0 : SCAL_TMA_TILE);  // multiple of 8
+        if (t == 0) {
+            mbar_arrive_expect_tx(&bar, (uint32_t)len * 4u);
+            bulk_g2s(buf, xb + f0, (uint32_t)len * 4u, &bar);
+        }
+        mbar_wait(&bar, phase);
+        for (int i = 4 * t; i < len; i += 4 * SCAL_TMA_T) {
+            float4 v = *reinterpret_cast<float4*>(buf + i);
+            v.x = __fmul_rn(alpha, v.x);
+            v.y = __fmul_rn(alpha, v.y);
+            v.z = __fmul_rn(alpha, v.z);
+            v.w = __fmul_rn(alpha, v.w);
+            *reinterpret_cast<float4*>(buf + i) = v;
+        }
+        fence_proxy_async_smem();  // the generic writes before the async-proxy read
+        __syncthreads();
+        if (t == 0) {
+            bulk_s2g(yb + f0, buf, (uint32_t)len * 4u);
+            bulk_commit_and_wait_read();  // buf is reused (or released) only after the read
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace lift

@@ -19,6 +19,9 @@ def child(reps=30):
     import lift_inputs as gen
     import paper_1502_02389_b200 as lift
     dev = torch.device("cuda:0")
+    for kv in filter(None, os.environ.get("LIFT_SET_VARIANTS", "").split(",")):
+        k, v = kv.split("=")
+        lift.set_variant(k, int(v))  # NEXT-4 runtime knobs (same build)
 
     def fill(n, tid, lo, hi):
         return gen.fill_device(torch.empty(n, dtype=torch.float32, device=dev), 0, tid, 0, 0, lo, hi)

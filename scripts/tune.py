@@ -40,15 +40,34 @@ SPACE = {
                   ("s256x4", "-DLIFT_SCAL_T=256 -DLIFT_SCAL_U=4")],
     "pdl": [("pdl_on", "-DLIFT_PDL=1"), ("pdl_off", "-DLIFT_PDL=0")],
     "ticket_fence": [("acq_rel", "-DLIFT_SC_FENCE=0"), ("sc_fence", "-DLIFT_SC_FENCE=1")],
+    # Fig. 7a/7b axes: the intra-warp tree in shared memory (toLocal +
+    # iterate(split-2 reduce), the paper's lowering) vs the shuffle butterfly — same bits
+    "tree": [("shuffle", "-DLIFT_TREE=1"), ("smem_tree", "-DLIFT_TREE=2")],
+    # vector width / load path: LDG.256 (default), LDG.128 and scalar via the RUNTIME knob
+    # (lift_set_variant LIFT_VAR_LOAD_WIDTH, same build), TMA bulk copies into shared memory
+    # for the map (scal) and the reductions (compile-time)
+    "load": [("ldg256", "", "load_width=8"), ("ldg128", "", "load_width=4"),
+             ("scalar", "", "load_width=1"), ("tma_bulk", "-DLIFT_SCAL_TMA=1 -DLIFT_RED_TMA=1")],
+    # gemv toLocal(x) strategies (RUNTIME knob LIFT_VAR_GEMV_X, same build): x through L1
+    # widened per use; x fp64 in shared memory + register ring; x fp64 in shared memory +
+    # TMA ring of A row segments (warp-specialised producer)
+    "gemv_x": [("x_l1", "", "gemv_x=1"), ("x_smem_regring", "", "gemv_x=2"),
+               ("x_smem_tmaring", "", "gemv_x=3")],
 }
 
 
 def variants():
-    vs = [("default", "")]
+    """(name, compile flags, runtime knobs); runtime-only points reuse the default build."""
+    vs = [("default", "", "")]
     for axis, pts in SPACE.items():
-        for name, flags in pts:
-            vs.append((f"{axis}={name}", flags))
+        for pt in pts:
+            name, flags = pt[0], pt[1]
+            vs.append((f"{axis}={name}", flags, pt[2] if len(pt) > 2 else ""))
     return vs
+
+
+def so_path(name, flags):
+    return os.path.join(OUT, (name.replace("=", "_") if flags else "default") + ".so")
 
 
 def build():
@@ -59,8 +78,10 @@ def build():
     src = os.path.join(ROOT, "paper_1502_02389_b200", "csrc", "lift.cu")
 
     def one(v):
-        name, flags = v
-        so = os.path.join(OUT, name.replace("=", "_") + ".so")
+        name, flags, _ = v
+        so = so_path(name, flags)
+        if not flags and name != "default":
+            return name, 0, ""
         r = subprocess.run(nv + flags.split() + [src, "-o", so], capture_output=True, text=True)
         return name, r.returncode, r.stderr[-500:]
 
@@ -72,20 +93,21 @@ def build():
 def measure(out_path=None):
     ab = os.path.join(ROOT, "scripts", "ab.py")
     results = {}
-    for name, flags in variants():
-        so = os.path.join(OUT, name.replace("=", "_") + ".so")
+    for name, flags, knobs in variants():
+        so = so_path(name, flags)
         if not os.path.exists(so):
             continue
-        env = dict(os.environ, LIFT_LIB=so)
+        env = dict(os.environ, LIFT_LIB=so, LIFT_SET_VARIANTS=knobs)
         r = subprocess.run([sys.executable, ab, "--child"], env=env, capture_output=True, text=True,
                            timeout=600)
         try:
-            results[name] = {"flags": flags, **json.loads(r.stdout.strip().splitlines()[-1])}
+            results[name] = {"flags": flags, "knobs": knobs,
+                             **json.loads(r.stdout.strip().splitlines()[-1])}
         except Exception:
-            results[name] = {"flags": flags, "error": r.stderr[-800:]}
+            results[name] = {"flags": flags, "knobs": knobs, "error": r.stderr[-800:]}
         print(name, json.dumps(results[name]), flush=True)
     best = {}
-    ops = sorted({k for v in results.values() for k in v if k not in ("flags", "error")})
+    ops = sorted({k for v in results.values() for k in v if k not in ("flags", "knobs", "error")})
     for op in ops:
         cand = [(v[op]["us"], n) for n, v in results.items() if op in v]
         if cand:
@@ -97,11 +119,48 @@ def measure(out_path=None):
         with open(out_path, "w") as f:
             json.dump(report, f, indent=1)
     print(json.dumps(best, indent=1))
+    if out_path:
+        with open(os.path.splitext(out_path)[0] + "_summary.txt", "w") as f:
+            f.write(summary(report))
+
+
+def summary(report):
+    """Fixed-width table: us per launch for every variant x op, then the winner per op and
+    per axis (the paper's 'chosen by exploring different values empirically')."""
+    res = report["results"]
+    ops = sorted({k for v in res.values() for k in v if k not in ("flags", "knobs", "error")})
+    lines = ["# NEXT-4 variant search (scripts/tune.py): us per launch (CUDA-graph replay of 30 "
+             "back-to-back launches, median of 5). One axis varied at a time; every variant "
+             "computes the same canonical order except red_k (a different chunk size).",
+             "variant".ljust(28) + "".join(o[:11].rjust(12) for o in ops)]
+    for n, v in res.items():
+        lines.append(n[:27].ljust(28) + "".join(
+            (f"{v[o]['us']:.2f}" if o in v else "-").rjust(12) for o in ops))
+    lines.append("")
+    lines.append("winner per op: " + json.dumps(report["best"]))
+    axes = {}
+    for n in res:
+        if "=" in n:
+            axes.setdefault(n.split("=")[0], []).append(n)
+    lines.append("")
+    lines.append("winner per axis and op (us; default in parentheses):")
+    for ax, names in axes.items():
+        row = []
+        for o in ops:
+            c = [(res[n][o]["us"], n.split("=")[1]) for n in names if o in res[n]]
+            if c:
+                us, w = min(c)
+                row.append(f"{o}:{w}({us:.2f}/{res['default'][o]['us']:.2f})")
+        lines.append(f"  {ax}: " + "  ".join(row))
+    return "\n".join(lines) + "\n"
 
 
 if __name__ == "__main__":
     if sys.argv[1:2] == ["build"]:
         build()
+    elif sys.argv[1:2] == ["summary"]:
+        with open(sys.argv[2]) as f:
+            print(summary(json.load(f)))
     elif sys.argv[1:2] == ["measure"]:
         measure(sys.argv[2] if len(sys.argv) > 2 else None)
     else:
