@@ -230,15 +230,22 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
  *   value 0 = the tuned default.  Unknown knob or value: LIFT_ERR_INVALID_VALUE.
  *     LIFT_VAR_LOAD_WIDTH  cap on the global load/store width: 0 auto (the widest the
  *                          alignment allows: LDG/STG.256), 1 scalar, 4 = 128-bit, 8 = 256-bit
- *     LIFT_VAR_GEMV_X      gemv rows of 2048..24576 columns: 0 auto, 1 x read through L1 and
- *                          widened per use, 2 x staged once per CTA as fp64 in shared memory
- *                          (persistent CTAs, Cluster Launch Control stealing)
+ *     LIFT_VAR_GEMV_X      gemv rows of 2048..24576 columns: 0 auto (= 1), 1 x read through L1
+ *                          and widened per use, 2 x staged once per CTA as fp64 in shared
+ *                          memory + a register ring of A (persistent CTAs, Cluster Launch
+ *                          Control stealing), 3 the same x staging + a TMA ring of A row
+ *                          segments fed by a producer warp (n <= 16384)
+ *     LIFT_VAR_PREFETCH    TMA L2 prefetch of a CTA's first unit at its start, before the PDL
+ *                          wait (overlaps the previous kernel's tail): 0 auto (scal: first
+ *                          wave; fused map+reduce: on; asum/dot: off; gemv: when the launch
+ *                          has >= 4 waves of row blocks), 1 off everywhere, 2 on everywhere
  *   (The other Fig. 7 axes — shared-memory tree vs shuffle butterfly, TMA bulk loads, chunk
  *   size — are compile-time variants searched by scripts/tune.py.) */
 typedef enum {
     LIFT_VAR_LOAD_WIDTH = 0,
     LIFT_VAR_GEMV_X = 1,
-    LIFT_VAR_COUNT = 2
+    LIFT_VAR_PREFETCH = 2,
+    LIFT_VAR_COUNT = 3
 } lift_variant;
 lift_status lift_set_variant(lift_variant knob, int value);
 int lift_get_variant(lift_variant knob);

@@ -181,6 +181,33 @@ __device__ __forceinline__ f8 ld_realigned(const float* p, int d, bool inner) {
 // attribute).  pdl_trigger() lets the NEXT kernel's CTAs be scheduled once every CTA of
 // this one has started (they then wait in their own pdl_wait()).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// L2 prefetch of [p, p + bytes) by the TMA engine (one instruction, no registers, no
+// completion to wait for).  Issued BEFORE pdl_wait() by the first CTAs of a kernel, it
+// overlaps their first DRAM round trip with the previous kernel's tail: L2 is the point of
+// coherence, so prefetching data the previous kernel may still write is harmless (its
+// stores update the L2 line; nothing is read into registers or L1 before the wait).
+// p must be 16-byte aligned; bytes is rounded down to a multiple of 16.
+#ifndef LIFT_PREFETCH
+#define LIFT_PREFETCH 7  // bit mask: 1 scal, 2 reductions, 4 gemv
+#endif
+// Only CTAs of the first resident wave (blockIdx < SMs x resident CTAs per SM) can start
+// while the previous kernel still drains; later CTAs would only duplicate their own loads.
+__device__ __forceinline__ bool in_first_wave(int per_sm) {
+    unsigned nsm;
+    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    return blockIdx.x < nsm * (unsigned)per_sm;
+}
+template <int WHO>
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+#if LIFT_PREFETCH
+    if constexpr ((LIFT_PREFETCH & WHO) == 0) return;
+    bytes &= ~(int64_t)15;
+    if (bytes <= 0 || (reinterpret_cast<uintptr_t>(p) & 15)) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)bytes)
+                 : "memory");
+#endif
+}
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }

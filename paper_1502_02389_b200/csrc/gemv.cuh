@@ -42,6 +42,9 @@ namespace lift {
 #ifndef LIFT_GEMV_B
 #define LIFT_GEMV_B 4     // vectors per thread in flight (launch shape only, not the order)
 #endif
+#ifndef LIFT_GEMV_PF_AHEAD
+#define LIFT_GEMV_PF_AHEAD 0
+#endif
 #ifndef LIFT_GEMV_XJIT
 #define LIFT_GEMV_XJIT 0  // 1: a thread's A batch issued before any x load (x loaded per use)
 #endif
@@ -66,6 +69,7 @@ struct GemvArgs {
     const float* y;
     float* y_out;
     int64_t nblocks;  // row blocks (of 256/TR rows) of this launch
+    int prefetch;     // L2-prefetch each block's rows at CTA start (many waves of blocks)
     // NEXT-1 fused all-gather of y (null y_peers: plain local y_out)
     float* const* y_peers;  // p pointers: every rank's full-length y (IPC-mapped)
     int64_t row0;           // global row of local row 0
@@ -270,6 +274,21 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
 
 template <int TRL, int LW, bool PEERS>
 __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
+    constexpr int RPB = GEMV_T >> TRL;  // rows per block
+    // With many waves of blocks, the TMA prefetch puts a block's whole rows in flight at
+    // once, more than the threads' register-bound load waves hold (8192^2: 43.2 -> 41.2 us);
+    // when every block is resident at once it only duplicates the loads (1024 x 8192: 8.1 ->
+    // 9.8 us), so the launcher enables it for >= 4 waves (scripts/gpu_r2_ab.sh)
+    if (a.prefetch && threadIdx.x < RPB && blockIdx.x < a.nblocks) {  // this CTA's first rows
+        const int64_t row = (int64_t)blockIdx.x * RPB + threadIdx.x;
+        if (row < a.m) prefetch_l2<4>(a.A + row * a.lda, a.n * 4);
+#if LIFT_GEMV_PF_AHEAD  // (A/B) also the rows of the CTA one resident wave later
+        unsigned nsm;
+        asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+        const int64_t r2 = row + (int64_t)nsm * GEMV_MINB * RPB;
+        if (r2 < a.m) prefetch_l2<4>(a.A + r2 * a.lda, a.n * 4);
+#endif
+    }
     pdl_wait();
     pdl_trigger();
     constexpr int TR = 1 << TRL;

@@ -94,6 +94,10 @@ __global__ void __launch_bounds__(GXS_T, LIFT_GXS_MINB) gemv_xs_kernel(GemvArgs 
     Clc clc{clc_resp, clc_bar, 0};
     if (t == 0) mbar_init(clc_bar, 1);
 
+    if ((t & ((1 << TRL) - 1)) == 0) {  // the first block's rows (common.cuh prefetch_l2)
+        const int64_t r = (int64_t)blockIdx.x * RP + (t >> TRL);
+        if (r < a.m) prefetch_l2<4>(a.A + r * a.lda, a.n * 4);
+    }
     pdl_wait();  // x, A, y may be the previous kernel's output
     pdl_trigger();
     // ---- G1: x -> fp64 shared memory, once per resident CTA -------------------------
@@ -130,12 +134,16 @@ __global__ void __launch_bounds__(GXS_T, LIFT_GXS_MINB) gemv_xs_kernel(GemvArgs 
         int64_t next = 0;
         bool more = false;
         const float* rpn = rp;
+        const int fetch_round = K > P ? P : 0;  // learn the next block one round in
         for (int k0 = 0; k0 < K; k0 += P) {
             const bool last_round = k0 + P == K;
 #if !LIFT_GXS_ONESHOT
-            if (last_round) {  // the next block: its loads go out before this row's tree
-                more = clc_fetch(clc, next);
-                if (more) rpn = row_ptr(next);
+            if (k0 == fetch_round) {  // the next block: L2-prefetch its rows now, and its
+                more = clc_fetch(clc, next);  // first ring loads go out before this row's tree
+                if (more) {
+                    rpn = row_ptr(next);
+                    if (tp == 0) prefetch_l2<4>(rpn, a.n * 4);
+                }
             }
 #endif
 #pragma unroll

@@ -267,6 +267,10 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     a.rank = xa.rank;
     a.epoch = xa.epoch;
     a.error = xa.error;
+    {
+        const int pf = var(LIFT_VAR_PREFETCH);
+        a.prefetch = pf == 2 || (pf == 0 && Op::kMapStore);
+    }
 
     uintptr_t al = reinterpret_cast<uintptr_t>(x);
     if (Op::kTwoInputs) al |= reinterpret_cast<uintptr_t>(y);
@@ -299,7 +303,9 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
 template <int LW, bool ALIAS>
 void scal_go(int64_t grid, int64_t nslots, int head, int tail, float alpha, const float* x,
              float* y, cudaStream_t s) {
-    launch(scal_kernel<LW, ALIAS>, grid, SCAL_T, LIFT_SCAL_SMEM, s, nslots, head, tail, alpha, x, y);
+    const int pf = var(LIFT_VAR_PREFETCH);
+    launch(scal_kernel<LW, ALIAS>, grid, SCAL_T, LIFT_SCAL_SMEM, s, nslots, head, tail, alpha, x, y,
+           pf == 1 ? 0 : 1);
 }
 
 template <int LW>
@@ -317,6 +323,9 @@ lift_status gemv_go(GemvArgs a, cudaStream_t s) {
     a.nblocks = (a.m + rp - 1) / rp;
     const void* fn = (const void*)gemv_kernel<TRL, LW, PEERS>;
     const int64_t grid = grid_for(a.nblocks, fn, GEMV_T, 0, LIFT_PERSISTENT);
+    const int dev = current_device();
+    const int pf = var(LIFT_VAR_PREFETCH);
+    a.prefetch = pf == 2 || (pf == 0 && a.nblocks >= 4 * (int64_t)sm_count(dev) * occupancy(fn, GEMV_T, 0));
     launch(gemv_kernel<TRL, LW, PEERS>, grid, GEMV_T, 0, s, a);
     return launched();
 }
@@ -507,6 +516,7 @@ lift_status lift_set_variant(lift_variant knob, int value) {
     switch (knob) {
         case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
         case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 3; break;
+        case LIFT_VAR_PREFETCH: ok = value >= 0 && value <= 2; break;
         default: break;
     }
     if (!ok) return LIFT_ERR_INVALID_VALUE;

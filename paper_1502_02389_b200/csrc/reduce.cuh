@@ -128,6 +128,7 @@ struct ReduceArgs {
     int p, rank;
     unsigned long long epoch;  // > 0, increasing per call on the same buffers
     int* error;                // set to 1 if the peers did not arrive in time
+    int prefetch;              // L2-prefetch the CTA's first chunk before the PDL wait
 };
 
 // ---- NEXT-1: the outermost reduce across GPUs, inside the kernel -------------------
@@ -477,6 +478,14 @@ __device__ __forceinline__ void trace_start(int64_t c) {
 // One CTA per chunk, hardware-scheduled (the default).
 template <class Op, int LW, int B>
 __global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
+    // the CTA's first chunk, L2-prefetched before the wait (common.cuh prefetch_l2); the
+    // launcher enables it for the fused map+store ops (LIFT_VAR_PREFETCH)
+    if (a.prefetch && threadIdx.x == 0 && blockIdx.x < a.nc) {
+        const int64_t b0 = (int64_t)blockIdx.x * RED_C;
+        const int64_t len = (a.n - b0 < RED_C ? a.n - b0 : RED_C) * 4;
+        prefetch_l2<2>(a.x + b0, len);
+        if constexpr (Op::kTwoInputs) prefetch_l2<2>(a.y + b0, len);
+    }
     pdl_wait();
     pdl_trigger();
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity

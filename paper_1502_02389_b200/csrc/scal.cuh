@@ -44,7 +44,14 @@ __device__ __forceinline__ f8 scal_load(const float* p) {
 // tail: elements [head + 8*nslots, head + 8*nslots + tail).
 template <int LW, bool ALIAS>
 __global__ void __launch_bounds__(SCAL_T) scal_kernel(int64_t nslots, int head, int tail,
-                                                      float alpha, const float* x, float* y) {
+                                                      float alpha, const float* x, float* y,
+                                                      int prefetch) {
+    // the first wave's tiles, L2-prefetched before the wait (common.cuh prefetch_l2)
+    if (prefetch && threadIdx.x == 0 && in_first_wave(2048 / SCAL_T)) {
+        const int64_t s0 = (int64_t)blockIdx.x * SCAL_T * SCAL_U;
+        const int64_t ns = nslots - s0 < (int64_t)SCAL_T * SCAL_U ? nslots - s0 : (int64_t)SCAL_T * SCAL_U;
+        if (ns > 0) prefetch_l2<1>(x + head + 8 * s0, ns * 32);
+    }
     pdl_wait();
     pdl_trigger();
     const int t = threadIdx.x;

@@ -45,7 +45,8 @@ def run_all(lift, off):
     return out
 
 
-@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3))])
+@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3)),
+                                         ("prefetch", (1, 2))])
 @pytest.mark.parametrize("off", [0, 4])
 def test_variants_bit_identical(lift, knob, values, off):
     ref = run_all(lift, off)
