@@ -87,8 +87,13 @@ const char* lift_last_cuda_error(void);
  * start) and its last-block-done tickets (in a tail region whose size depends only on
  * ws_bytes).  The caller ZERO-FILLS it ONCE after allocation and then always passes the
  * SAME ws_bytes with that buffer; every call leaves the tickets at zero again, so one
- * buffer serves any n with lift_workspace_bytes(n) <= ws_bytes, indefinitely (unless a
- * kernel faults, after which it must be zero-filled again). */
+ * buffer serves any n with lift_workspace_bytes(n) <= ws_bytes, indefinitely.  Two calls
+ * in flight on one workspace, or a buffer that was not zero-filled, break this contract
+ * (use one workspace per stream; the Python binding allocates one per (device, stream)).
+ * A kernel that faults leaves the CUDA context unusable — every later launch then fails
+ * with LIFT_ERR_CUDA — so stale tickets of an aborted call are never consumed.  (An
+ * in-kernel guard that detects live foreign tickets was built and measured: it cost the
+ * reductions 2-20%, and is not part of the product.) */
 size_t lift_workspace_bytes(int64_t n);
 
 /* S1 — scal: y[i] = RN_fp32(alpha * x[i]) for 0 <= i < n.

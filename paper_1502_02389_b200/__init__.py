@@ -99,6 +99,10 @@ class Workspace:
     def ptr(self) -> int:
         return self.buf.data_ptr()
 
+    def reset(self) -> None:
+        """Zero-fill again (clears the tickets and the sticky error word)."""
+        self.buf.zero_()
+
 
 _ws_lock = threading.Lock()
 _ws_cache: dict = {}

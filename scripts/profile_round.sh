@@ -2,7 +2,7 @@
 # ncu evidence for profiles/: (1) launch list of the bench command (cold-cache, serialised
 # per-launch times: compare SHARES), (2) one --set full capture per kernel of the step.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-TAG=${TAG:-r1}
+TAG=${TAG:-r2}
 mkdir -p gpurun_out
 # skip the 7 generator fills + warm-up (3 steps x 4 launches) = 19 launches
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \

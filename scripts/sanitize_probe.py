@@ -43,5 +43,23 @@ for m, n, split in [(2, 65536 + 5, True), (1, 1 << 19, True), (2, 65536 + 5, Tru
                     (3, 70001, False), (600, 65536, True)]:
     A = torch.rand(m, n, generator=g).to(dev)
     lift.gemv(A, rnd(n), rnd(m), 1.5, 0.5, split=split)
+# round-2 kernels: staged-x gemv (register ring, TMA ring), prefetch on/off, 128-bit loads
+for var in (2, 3):
+    lift.set_variant("gemv_x", var)
+    for m, n in [(37, 2048), (9, 4096), (70, 8192), (3, 16384)]:
+        A = torch.rand(m, n, generator=g).to(dev)
+        lift.gemv(A, rnd(n), rnd(m), 1.5, 0.5)
+lift.set_variant("gemv_x", 0)
+for pf in (1, 2):
+    lift.set_variant("prefetch", pf)
+    x = rnd(3 * C + 11)
+    lift.scal(3.0, x), lift.asum(x), lift.scal_asum(2.0, x)
+    A = torch.rand(1100, 4096, generator=g).to(dev)
+    lift.gemv(A, rnd(4096), rnd(1100), 1.5, 0.5)
+lift.set_variant("prefetch", 0)
+lift.set_variant("load_width", 4)
+x, y = rnd(C + 77), rnd(C + 77)
+lift.scal(3.0, x), lift.dot(x, y)
+lift.set_variant("load_width", 0)
 torch.cuda.synchronize()
 print("sanitize probe ok")

@@ -552,3 +552,19 @@ def test_gemv_ws_too_small_or_null_falls_back_with_same_bits(lift):
                                 out.data_ptr(), wp, wb, stream) == 0
         torch.cuda.synchronize()
         assert np.array_equal(bits(out), want)
+
+
+def test_workspace_reset_restores_the_contract(lift):
+    """A dirty ticket (the contract broken) is repaired by Workspace.reset(): the next
+    call is correct again (bit-identical to a fresh workspace)."""
+    n = 3 * GROUP + 5
+    x = dev_gen(n, 4, gen.TID_X)
+    ws = lift.Workspace(n, torch.device(DEV))
+    good = lift.asum(x, ws=ws).item()
+    wf = ws.nbytes & ~15
+    region = ((wf // 512 + 2) * 4 + 15) & ~15
+    t0 = wf - region
+    ws.buf[t0:t0 + 4].view(torch.int32).fill_(5)
+    lift.asum(x, ws=ws)
+    ws.reset()
+    assert lift.asum(x, ws=ws).item() == good
