@@ -45,9 +45,6 @@ namespace lift {
 #ifndef LIFT_GEMV_PF_AHEAD
 #define LIFT_GEMV_PF_AHEAD 0
 #endif
-#ifndef LIFT_GEMV_XJIT
-#define LIFT_GEMV_XJIT 0  // 1: a thread's A batch issued before any x load (x loaded per use)
-#endif
 #ifndef LIFT_GEMV_EXPT
 #define LIFT_GEMV_EXPT 0  // timing experiments only (scripts/gpu_r2_gemv.sh); never the product
 #endif
@@ -94,29 +91,6 @@ __device__ __forceinline__ double f2d_bits(float f) {
     const unsigned u = __float_as_uint(f);
     const unsigned hi = (((u >> 3) & 0x0FFFFFFFu) | (u & 0x80000000u)) + 0x38000000u;
     return __hiloint2double((int)hi, (int)(u << 29));
-}
-
-// Ordered (volatile) forms for LIFT_GEMV_XJIT: keep the A batch ahead of the x loads.
-template <int LW>
-__device__ __forceinline__ f8 ld_slot_vol(const float* p) {
-    if constexpr (LW == 8) {
-        f8 r;
-        asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
-                       "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
-                     : "l"(p));
-        return r;
-    } else {
-        return ld_slot<LW>(p);
-    }
-}
-__device__ __forceinline__ f8 ld_x_vol(const float* p) {
-    f8 r;
-    asm volatile("ld.global.nc.L1::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
-                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
-                 : "l"(p));
-    return r;
 }
 
 // x through L1: one copy per SM serves every resident CTA (G1).
@@ -190,24 +164,6 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
     constexpr int LX = RA ? 8 : LW;
     const int dxo = LW == 3 ? (int)((reinterpret_cast<uintptr_t>(a.x) >> 2) & 7) : 0;
     int64_t k = 0;
-#if LIFT_GEMV_XJIT
-    if constexpr (!RA) {
-        // A batch first (all B loads in flight), then x just in time per vector (an L1
-        // hit), so x never holds registers across the DRAM wait
-        for (; (k + B) * TR <= nv; k += B) {
-            f8 av[B];
-#pragma unroll
-            for (int b = 0; b < B; ++b) av[b] = ld_slot_vol<LW>(rp + 8 * (tp + (k + b) * TR));
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const f8 xv = ld_x_vol(a.x + 8 * (tp + (k + b) * TR));
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    acc[e] = __fma_rn((double)av[b].v[e], (double)xv.v[e], acc[e]);
-            }
-        }
-    }
-#endif
     for (; (k + B) * TR <= nv; k += B) {  // full batches: every vector in range
         f8 av[B], xv[B];
 #pragma unroll
