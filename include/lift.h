@@ -244,13 +244,19 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
  *                          wait (overlaps the previous kernel's tail): 0 auto (scal: first
  *                          wave; fused map+reduce: on; asum/dot: off; gemv: when the launch
  *                          has >= 4 waves of row blocks), 1 off everywhere, 2 on everywhere
+ *     LIFT_VAR_ORDER       temporal order in which asum/dot visit their chunks (the summation
+ *                          order is by chunk index either way): 0 auto (descending, so a
+ *                          reduction after a map over the same vector starts on the tail the
+ *                          map left in L2; the fused map+reduce ascending), 1 ascending,
+ *                          2 descending
  *   (The other Fig. 7 axes — shared-memory tree vs shuffle butterfly, TMA bulk loads, chunk
  *   size — are compile-time variants searched by scripts/tune.py.) */
 typedef enum {
     LIFT_VAR_LOAD_WIDTH = 0,
     LIFT_VAR_GEMV_X = 1,
     LIFT_VAR_PREFETCH = 2,
-    LIFT_VAR_COUNT = 3
+    LIFT_VAR_ORDER = 3,
+    LIFT_VAR_COUNT = 4
 } lift_variant;
 lift_status lift_set_variant(lift_variant knob, int value);
 int lift_get_variant(lift_variant knob);

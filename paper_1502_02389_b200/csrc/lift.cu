@@ -214,6 +214,17 @@ struct XchgArgs {  // NEXT-1: in-kernel cross-GPU combine (all null: single GPU)
 #define LIFT_REDUCE_REALIGN 1  // 4-byte-aligned asum/dot operands: realigned 256-bit loads
 #endif
 
+// One launch of reduce_kernel (the 128-/256-bit classes; DESC: chunks visited in
+// descending order, reduce.cuh).
+template <class Op, int LW, int B, bool DESC>
+lift_status reduce_go(const ReduceArgs& a, int64_t nc, cudaStream_t stream) {
+    const size_t tsm = (LIFT_RED_TMA && !Op::kMapStore) ? (size_t)RED_C * 4 * (Op::kTwoInputs ? 2 : 1) : 0;
+    const void* fn = (const void*)reduce_kernel<Op, LW, B, DESC>;
+    const int64_t grid = grid_for(nc, fn, RED_T, tsm, LIFT_PERSISTENT);
+    launch(reduce_kernel<Op, LW, B, DESC>, grid, RED_T, tsm, stream, a);
+    return launched();
+}
+
 template <class Op, int B>
 lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out32, double* out64,
                           void* ws, size_t ws_bytes, cudaStream_t stream, float alpha = 0.f,
@@ -271,6 +282,8 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
         const int pf = var(LIFT_VAR_PREFETCH);
         a.prefetch = pf == 2 || (pf == 0 && Op::kMapStore);
     }
+    const int ord = var(LIFT_VAR_ORDER);
+    const bool desc = ord == 2 || (ord == 0 && !Op::kMapStore);
 
     uintptr_t al = reinterpret_cast<uintptr_t>(x);
     if (Op::kTwoInputs) al |= reinterpret_cast<uintptr_t>(y);
@@ -281,6 +294,8 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
         if (lw == 1 && LIFT_REDUCE_REALIGN && !lw_capped()) lw = 2;
     }
     lw = lw == 2 ? 2 : cap_lw(lw);
+    if (desc && lw == 8) return reduce_go<Op, 8, B, true>(a, L.nc, stream);
+    if (desc && lw == 4) return reduce_go<Op, 4, B, true>(a, L.nc, stream);
     const void* fn = lw == 8 ? (const void*)reduce_kernel<Op, 8, B>
                    : lw == 4 ? (const void*)reduce_kernel<Op, 4, B>
                    : lw == 2 ? (const void*)reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>
@@ -517,6 +532,7 @@ lift_status lift_set_variant(lift_variant knob, int value) {
         case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
         case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 3; break;
         case LIFT_VAR_PREFETCH: ok = value >= 0 && value <= 2; break;
+        case LIFT_VAR_ORDER: ok = value >= 0 && value <= 2; break;
         default: break;
     }
     if (!ok) return LIFT_ERR_INVALID_VALUE;

@@ -476,12 +476,12 @@ __device__ __forceinline__ void trace_start(int64_t c) {
 }
 
 // One CTA per chunk, hardware-scheduled (the default).
-template <class Op, int LW, int B>
+template <class Op, int LW, int B, bool DESC = false>
 __global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBlocks) reduce_kernel(ReduceArgs a) {
     // the CTA's first chunk, L2-prefetched before the wait (common.cuh prefetch_l2); the
     // launcher enables it for the fused map+store ops (LIFT_VAR_PREFETCH)
     if (a.prefetch && threadIdx.x == 0 && blockIdx.x < a.nc) {
-        const int64_t b0 = (int64_t)blockIdx.x * RED_C;
+        const int64_t b0 = (DESC ? a.nc - 1 - (int64_t)blockIdx.x : (int64_t)blockIdx.x) * RED_C;
         const int64_t len = (a.n - b0 < RED_C ? a.n - b0 : RED_C) * 4;
         prefetch_l2<2>(a.x + b0, len);
         if constexpr (Op::kTwoInputs) prefetch_l2<2>(a.y + b0, len);
@@ -497,7 +497,13 @@ __global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBloc
         __syncthreads();
     }
     int parity = 0;
-    for (int64_t c = blockIdx.x; c < a.nc; c += gridDim.x, parity ^= 1) {
+    // Temporal order of the chunks (never the summation order: partials are stored and
+    // folded by chunk INDEX, so the bits are the same either way).  Descending lets a
+    // reduction that follows a map over the same vector (scal, then asum of its input)
+    // start where the map ended — on the tail the map just left in the 126 MB L2.
+    const int64_t cstep = DESC ? -(int64_t)gridDim.x : (int64_t)gridDim.x;
+    for (int64_t c = DESC ? a.nc - 1 - blockIdx.x : blockIdx.x; DESC ? c >= 0 : c < a.nc;
+         c += cstep, parity ^= 1) {
         trace_start(c);
         // ---- R1/R2: fused per-lane fold over the chunk ---------------------------
         const int64_t base = c * RED_C;

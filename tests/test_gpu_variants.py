@@ -46,7 +46,7 @@ def run_all(lift, off):
 
 
 @pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3)),
-                                         ("prefetch", (1, 2))])
+                                         ("prefetch", (1, 2)), ("order", (1, 2))])
 @pytest.mark.parametrize("off", [0, 4])
 def test_variants_bit_identical(lift, knob, values, off):
     ref = run_all(lift, off)
