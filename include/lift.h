@@ -239,7 +239,8 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
  *                          and widened per use, 2 x staged once per CTA as fp64 in shared
  *                          memory + a register ring of A (persistent CTAs, Cluster Launch
  *                          Control stealing), 3 the same x staging + a TMA ring of A row
- *                          segments fed by a producer warp (n <= 16384)
+ *                          segments fed by a producer warp (n <= 16384), 4 two rows per
+ *                          thread: each x vector loaded and widened once for both
  *     LIFT_VAR_PREFETCH    TMA L2 prefetch of a CTA's first unit at its start, before the PDL
  *                          wait (overlaps the previous kernel's tail): 0 auto (scal: first
  *                          wave; fused map+reduce: on; asum/dot: off; gemv: when the launch

@@ -16,6 +16,7 @@
 #include "gemv.cuh"
 #include "gemv_xs.cuh"
 #include "gemv_tma.cuh"
+#include "gemv_r2.cuh"
 #include "reduce.cuh"
 #include "gemv_long.cuh"
 #include "scal.cuh"
@@ -406,6 +407,29 @@ lift_status gtm_trl(const GemvArgs& a, int nst, cudaStream_t s) {
     }
 }
 
+template <int TRL, int LW>
+lift_status gr2_go(GemvArgs a, cudaStream_t s) {
+    constexpr int T = gr2_threads(TRL);
+    constexpr int64_t rb = 2 * (T >> TRL);  // rows per block
+    a.nblocks = (a.m + rb - 1) / rb;
+    const void* fn = (const void*)gemv_r2_kernel<TRL, LW>;
+    const int64_t grid = grid_for(a.nblocks, fn, T, 0, LIFT_PERSISTENT);
+    const int pf = var(LIFT_VAR_PREFETCH);
+    a.prefetch = pf == 2 || (pf == 0 && a.nblocks >= 4 * (int64_t)sm_count(current_device()) *
+                                                         occupancy(fn, T, 0));
+    launch(gemv_r2_kernel<TRL, LW>, grid, T, 0, s, a);
+    return launched();
+}
+
+lift_status gr2_trl(const GemvArgs& a, int lw, cudaStream_t s) {
+    switch (gemv_tr_log2(a.n)) {  // n >= 2048: 32..256 threads per row
+        case 8: return lw == 8 ? gr2_go<8, 8>(a, s) : gr2_go<8, 4>(a, s);
+        case 7: return lw == 8 ? gr2_go<7, 8>(a, s) : gr2_go<7, 4>(a, s);
+        case 6: return lw == 8 ? gr2_go<6, 8>(a, s) : gr2_go<6, 4>(a, s);
+        default: return lw == 8 ? gr2_go<5, 8>(a, s) : gr2_go<5, 4>(a, s);
+    }
+}
+
 int smem_optin(int dev) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -483,6 +507,8 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
     // threads, aligned, and enough of them to amortise one x staging per resident CTA
     // (gemv_xs.cuh)
     const int gx = var(LIFT_VAR_GEMV_X);
+    if (gx == 4 && lw >= 4 && !a.y_peers && gr2_shape_ok(a.n))  // two rows per thread
+        return gr2_trl(a, lw, s);
     if (gx == 3 && lw >= 4 && gtm_shape_ok(a.n)) {  // TMA ring (gemv_tma.cuh)
         const int nst = gtm_stages(a.n, (size_t)smem_optin(current_device()));
         if (nst >= 2) return a.y_peers ? gtm_trl<true>(a, nst, s) : gtm_trl<false>(a, nst, s);
@@ -530,7 +556,7 @@ lift_status lift_set_variant(lift_variant knob, int value) {
     bool ok = false;
     switch (knob) {
         case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
-        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 3; break;
+        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 4; break;
         case LIFT_VAR_PREFETCH: ok = value >= 0 && value <= 2; break;
         case LIFT_VAR_ORDER: ok = value >= 0 && value <= 2; break;
         default: break;

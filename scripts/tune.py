@@ -52,7 +52,7 @@ SPACE = {
     # widened per use; x fp64 in shared memory + register ring; x fp64 in shared memory +
     # TMA ring of A row segments (warp-specialised producer)
     "gemv_x": [("x_l1", "", "gemv_x=1"), ("x_smem_regring", "", "gemv_x=2"),
-               ("x_smem_tmaring", "", "gemv_x=3")],
+               ("x_smem_tmaring", "", "gemv_x=3"), ("x_two_rows", "", "gemv_x=4")],
 }
 
 

@@ -45,7 +45,7 @@ def run_all(lift, off):
     return out
 
 
-@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3)),
+@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3, 4)),
                                          ("prefetch", (1, 2)), ("order", (1, 2))])
 @pytest.mark.parametrize("off", [0, 4])
 def test_variants_bit_identical(lift, knob, values, off):
@@ -59,10 +59,11 @@ def test_variants_bit_identical(lift, knob, values, off):
         lift.set_variant(knob, 0)
 
 
-@pytest.mark.parametrize("var", [2, 3])
+@pytest.mark.parametrize("var", [2, 3, 4])
 def test_staged_x_gemv_matches_oracle(lift, var):
-    """The staged-x kernels (LIFT_VAR_GEMV_X = 2: register ring; 3: TMA ring) against the
-    oracle directly, with a partial last row block and signed inputs."""
+    """The gemv x-strategy kernels (LIFT_VAR_GEMV_X = 2: x in shared memory + register ring;
+    3: + TMA ring; 4: two rows per thread) against the oracle directly, with a partial last
+    row block and signed inputs."""
     lift.set_variant("gemv_x", var)
     for m, n in ((1001, 8192), (65, 4096), (3, 16384), (37, 2048)):
         A = gen.host(m * n, 7, gen.TID_A).reshape(m, n)
