@@ -118,33 +118,45 @@ __device__ __forceinline__ f8 ld_x(const float* p) {
     }
 }
 
-// NEXT-1 fused all-gather: a CTA counts the row blocks it finished in this rank's
-// exchange buffer (one system fence and one atomic per count; the persistent gemv_xs
-// kernel counts once per CTA, gemv_kernel once per block); the CTA that completes the
-// count publishes the rank's flag into every peer's buffer (system-scope release) and
-// waits for all p flags, so the kernel ends only when every rank's rows have landed in
-// this rank's y — stream-ordered consumers can read it.  Called by warp 0 after a CTA
-// barrier that follows the CTA's row stores.
+// NEXT-1 fused all-gather: every CTA adds the number of row blocks it finished to this
+// rank's counter (`red.release.gpu`: fire-and-forget, so no CTA holds its slot waiting for
+// an atomic's reply — with a returning atomic per CTA the 8192^2 gemv ran 40% slower, and
+// a per-CTA __threadfence_system cost as much, scripts/xchg_p1.py).  The release orders
+// the CTA's row stores — local and remote, by any of its threads before the barrier that
+// precedes the call — before its count.  ONE CTA, the last of the grid (the last to be
+// scheduled, so it waits least; any other CTA can still run, so waiting cannot deadlock),
+// acquires the counter until every block is counted, resets it, publishes the rank's
+// flag into every peer's buffer (system-scope release: cumulative, so it carries every
+// counted CTA's stores) and waits for all p flags: the kernel ends only when every rank's
+// rows have landed in this rank's y.  Called by warp 0 after a CTA barrier.
 __device__ __forceinline__ void gemv_cta_done(const GemvArgs& a, int64_t count) {
     const int lane = threadIdx.x & 31;
     const int bank = (int)(a.epoch & 1ull);
-    unsigned last = 0;
-    if (lane == 0) {
-        __threadfence_system();  // the CTA's row stores (ordered by the barrier) before its count
-        unsigned long long* cnt = xchg_counter(a.xpeers[a.rank], a.p, bank);
-        last = (atomicAdd(cnt, (unsigned long long)count) + (unsigned long long)count ==
-                (unsigned long long)a.nblocks);
-        if (last) {
-            __threadfence_system();
-            *cnt = 0ull;  // reset for epoch + 2 (this bank's next use)
-        }
-    }
-    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    unsigned long long* cnt = xchg_counter(a.xpeers[a.rank], a.p, bank);
+    if (lane == 0 && count > 0)
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(cnt),
+                     "l"((unsigned long long)count)
+                     : "memory");
+    if (blockIdx.x != gridDim.x - 1) return;
     bool ok = true;
+    if (lane == 0) {  // bounded wait (~10 s), like the flag wait
+        unsigned long long v, spins = 0;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+            if (v >= (unsigned long long)a.nblocks) break;
+            __nanosleep(64);
+            if (++spins > (1ull << 27)) {
+                ok = false;
+                break;
+            }
+        }
+        *cnt = 0ull;  // reset for epoch + 2 (its next use is a later kernel)
+    }
+    __syncwarp();  // lane 0's acquire before every lane's release below
     if (lane < a.p) {
         XchgSlot* dst = reinterpret_cast<XchgSlot*>(a.xpeers[lane]) + bank * a.p + a.rank;
         st_release_sys(&dst->flag, a.epoch);
-        ok = xchg_wait_flag(a.xpeers[a.rank], bank * a.p, lane, a.epoch);
+        ok = xchg_wait_flag(a.xpeers[a.rank], bank * a.p, lane, a.epoch) && ok;
     }
     if (!__all_sync(0xffffffffu, ok) && lane == 0 && a.error) *a.error = 1;
 }
@@ -250,7 +262,12 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
     constexpr int TR = 1 << TRL;
     constexpr int RP = GEMV_T / TR;  // rows per block
     __shared__ double wv[2][GEMV_T / 32];  // warp values, double-buffered by block parity
+    __shared__ float* ypeer[PEERS ? 32 : 1];  // NEXT-1: the p peer y pointers, loaded once
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if constexpr (PEERS) {  // off the row path: a row store then needs no pointer load
+        if (t < a.p) ypeer[t] = a.y_peers[t];
+        __syncthreads();
+    }
     const int tp = t & (TR - 1);  // thread within its row
     const int64_t nv = a.n / 8;   // full vectors per row
     const int tailn = (int)(a.n & 7);
@@ -287,14 +304,18 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
             const double yb = __dmul_rn((double)a.beta, (double)a.y[row]);  // scal(b, y): exact
             const float out = __double2float_rn(__fma_rn((double)a.alpha, d, yb));
             if constexpr (PEERS) {  // fused all-gather: the row lands in every rank's full y
-                for (int q = 0; q < a.p; ++q) a.y_peers[q][a.row0 + row] = out;
+                for (int q = 0; q < a.p; ++q) ypeer[q][a.row0 + row] = out;
             } else {
                 a.y_out[row] = out;
             }
         }
-        if constexpr (PEERS) {
-            __syncthreads();  // every row store of this block precedes its count
-            if (warp == 0) gemv_cta_done(a, 1);
+    }
+    if constexpr (PEERS) {  // once per CTA, after its blocks (the loop stays the plain kernel's)
+        __syncthreads();  // every row store of this CTA precedes its count
+        if (warp == 0) {
+            const int64_t mine = blockIdx.x < a.nblocks
+                                     ? (a.nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+            gemv_cta_done(a, mine);
         }
     }
 }

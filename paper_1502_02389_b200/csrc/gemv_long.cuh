@@ -88,9 +88,12 @@ __global__ void __launch_bounds__(RED_T, 4) gemv_long_kernel(GemvArgs a) {
             }
         }
         if (t == 0) gemv_row_out(a, row, ng > 1 ? gs.close() : gp, PEERS);
-        if constexpr (PEERS) {
-            __syncthreads();  // the row store precedes the block count
-            if (warp == 0) gemv_cta_done(a, 1);
+    }
+    if constexpr (PEERS) {  // once per CTA, after its rows
+        __syncthreads();  // every row store of this CTA precedes its count
+        if (warp == 0) {
+            const int64_t mine = blockIdx.x < a.m ? (a.m - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+            gemv_cta_done(a, mine);
         }
     }
 }

@@ -147,8 +147,7 @@ __device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) 
     if (lane < a.p) {
         XchgSlot* dst = reinterpret_cast<XchgSlot*>(a.peers[lane]) + bank + a.rank;
         dst->value = total;
-        __threadfence_system();
-        st_release_sys(&dst->flag, a.epoch);
+        st_release_sys(&dst->flag, a.epoch);  // the release orders the value store before it
     }
     double v = 0.0;
     bool ok = true;
