@@ -235,8 +235,10 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
  *   value 0 = the tuned default.  Unknown knob or value: LIFT_ERR_INVALID_VALUE.
  *     LIFT_VAR_LOAD_WIDTH  cap on the global load/store width: 0 auto (the widest the
  *                          alignment allows: LDG/STG.256), 1 scalar, 4 = 128-bit, 8 = 256-bit
- *     LIFT_VAR_GEMV_X      gemv rows of 2048..24576 columns: 0 auto (= 1), 1 x read through L1
- *                          and widened per use, 2 x staged once per CTA as fp64 in shared
+ *     LIFT_VAR_GEMV_X      gemv rows of 2048..24576 columns: 0 auto (5 when the launch has
+ *                          >= 4 waves of row blocks and n <= 12288, else 1), 1 x read through
+ *                          L1 and widened per use, 5 x bulk-copied (TMA) into shared memory
+ *                          per CTA as fp32 and read from there, 2 x staged once per CTA as fp64 in shared
  *                          memory + a register ring of A (persistent CTAs, Cluster Launch
  *                          Control stealing), 3 the same x staging + a TMA ring of A row
  *                          segments fed by a producer warp (n <= 16384), 4 two rows per

@@ -165,9 +165,22 @@ __device__ __forceinline__ void gemv_cta_done(const GemvArgs& a, int64_t count) 
 // PEERS = the NEXT-1 fused all-gather (its code in the block loop costs the plain kernel
 // ~20% through worse load scheduling, so it is a separate instantiation).
 // One row's slot accumulators (thread tp of TR): the canonical order of gemv.cuh.
-template <int TRL, int LW>
+// XS (LIFT_VAR_GEMV_X = 5): x was bulk-copied into shared memory (xsm, fp32) by the TMA
+// engine at CTA start; the first batch's A loads go out before the wait for it.
+__device__ __forceinline__ f8 ld_x_smem(const float* xsm, int64_t q) {
+    const float4 u = reinterpret_cast<const float4*>(xsm)[2 * q];
+    const float4 w = reinterpret_cast<const float4*>(xsm)[2 * q + 1];
+    f8 r;
+    r.v[0] = u.x; r.v[1] = u.y; r.v[2] = u.z; r.v[3] = u.w;
+    r.v[4] = w.x; r.v[5] = w.y; r.v[6] = w.z; r.v[7] = w.w;
+    return r;
+}
+
+template <int TRL, int LW, bool XS = false>
 __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp, int tp, int lane,
-                                             int64_t nv, int tailn, double (&acc)[8]) {
+                                             int64_t nv, int tailn, double (&acc)[8],
+                                             const float* xsm = nullptr, uint64_t* xbar = nullptr,
+                                             bool* xready = nullptr) {
     constexpr int TR = 1 << TRL;
     constexpr int B = (LW == 2 || LW == 3) ? 2 : GEMV_B;  // realigned rows: 2 (4 spills; measured)
     const int d = (LW == 2 || LW == 3) ? (int)((reinterpret_cast<uintptr_t>(rp) >> 2) & 7) : 0;
@@ -176,6 +189,24 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
     constexpr int LX = RA ? 8 : LW;
     const int dxo = LW == 3 ? (int)((reinterpret_cast<uintptr_t>(a.x) >> 2) & 7) : 0;
     int64_t k = 0;
+    if constexpr (XS && !RA) {  // x from shared memory (loaded just in time, LDS)
+        for (; (k + B) * TR <= nv; k += B) {
+            f8 av[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) av[b] = ld_slot<LW>(rp + 8 * (tp + (k + b) * TR));
+            if (!*xready) {
+                mbar_wait(xbar, 0);
+                *xready = true;
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const f8 xv = ld_x_smem(xsm, tp + (k + b) * TR);
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    acc[e] = __fma_rn((double)av[b].v[e], (double)xv.v[e], acc[e]);
+            }
+        }
+    }
     for (; (k + B) * TR <= nv; k += B) {  // full batches: every vector in range
         f8 av[B], xv[B];
 #pragma unroll
@@ -240,7 +271,7 @@ __device__ __forceinline__ void gemv_row_acc(const GemvArgs& a, const float* rp,
     }
 }
 
-template <int TRL, int LW, bool PEERS>
+template <int TRL, int LW, bool PEERS, bool XS = false>
 __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
     constexpr int RPB = GEMV_T >> TRL;  // rows per block
     // With many waves of blocks, the TMA prefetch puts a block's whole rows in flight at
@@ -264,6 +295,17 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
     __shared__ double wv[2][GEMV_T / 32];  // warp values, double-buffered by block parity
     __shared__ float* ypeer[PEERS ? 32 : 1];  // NEXT-1: the p peer y pointers, loaded once
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    extern __shared__ __align__(128) unsigned char gemv_dsm[];
+    __shared__ __align__(8) uint64_t xbar;
+    bool xready = false;
+    if constexpr (XS) {  // x -> shared memory by one TMA bulk copy (n % 4 == 0, 16-B aligned)
+        if (t == 0) {
+            mbar_init(&xbar, 1);
+            mbar_arrive_expect_tx(&xbar, (uint32_t)(a.n * 4));
+            bulk_g2s(gemv_dsm, a.x, (uint32_t)(a.n * 4), &xbar);
+        }
+        __syncthreads();  // the barrier initialised before anyone waits on it
+    }
     if constexpr (PEERS) {  // off the row path: a row store then needs no pointer load
         if (t < a.p) ypeer[t] = a.y_peers[t];
         __syncthreads();
@@ -279,7 +321,8 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
         double acc[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-        gemv_row_acc<TRL, LW>(a, rp, tp, lane, nv, tailn, acc);
+        gemv_row_acc<TRL, LW, XS>(a, rp, tp, lane, nv, tailn, acc,
+                                  reinterpret_cast<const float*>(gemv_dsm), &xbar, &xready);
         double d;
         if constexpr (TR < 32) {
             // rows narrower than a warp: butterfly over the row's TR lanes only (xor stays

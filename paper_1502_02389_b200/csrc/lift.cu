@@ -105,11 +105,11 @@ int occupancy(const void* fn, int threads, size_t smem) {
             return g_occ[i].blocks;
     // The attribute is a per-function maximum: set it to the device's opt-in maximum, so
     // launches with any dynamic smem size (other n) stay valid whatever the call order.
-    if (smem > 48 * 1024) {  // the opt-in maximum minus the kernel's static shared memory
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, fn);
+    if (smem + fa.sharedSizeBytes > 48 * 1024) {  // opt-in maximum minus the static smem
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, fn);
         const int room = optin - (int)fa.sharedSizeBytes;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              room > (int)smem ? room : (int)smem);
@@ -346,6 +346,20 @@ lift_status gemv_go(GemvArgs a, cudaStream_t s) {
     return launched();
 }
 
+template <int TRL, int LW>
+lift_status gxsm_go(GemvArgs a, cudaStream_t s) {
+    constexpr int64_t rp = GEMV_T >> TRL;  // rows per block
+    a.nblocks = (a.m + rp - 1) / rp;
+    const size_t smem = (size_t)a.n * 4;
+    const void* fn = (const void*)gemv_kernel<TRL, LW, false, true>;
+    const int64_t grid = grid_for(a.nblocks, fn, GEMV_T, smem, LIFT_PERSISTENT);
+    const int pf = var(LIFT_VAR_PREFETCH);
+    a.prefetch = pf == 2 || (pf == 0 && a.nblocks >= 4 * (int64_t)sm_count(current_device()) *
+                                                         occupancy(fn, GEMV_T, smem));
+    launch(gemv_kernel<TRL, LW, false, true>, grid, GEMV_T, smem, s, a);
+    return launched();
+}
+
 template <int TRL, bool PEERS>
 lift_status gemv_lw(const GemvArgs& a, int lw, cudaStream_t s) {
     if (lw == 2) return gemv_go<TRL, 2, PEERS>(a, s);
@@ -509,6 +523,25 @@ lift_status gemv_launch(const GemvArgs& a, cudaStream_t s, void* ws = nullptr,
     const int gx = var(LIFT_VAR_GEMV_X);
     if (gx == 4 && lw >= 4 && !a.y_peers && gr2_shape_ok(a.n))  // two rows per thread
         return gr2_trl(a, lw, s);
+    // x bulk-copied into shared memory per CTA (gemv_kernel XS): with many waves of blocks
+    // the first batch's four A loads go out at once (x holds no registers across the DRAM
+    // wait): 8192^2 42.3 -> 40.7 us, 16384 x 8192 79.6 -> 76.8 us; with few waves the extra
+    // x traffic per CTA costs more than it saves (4096^2 13.6 -> 14.2 us), so auto requires
+    // >= 4 waves
+    bool xs = gx == 5;
+    if (gx == 0 && lw >= 4 && !a.y_peers && a.n >= 2048 && a.n <= 12288 && a.n % 4 == 0) {
+        const int trl = gemv_tr_log2(a.n);
+        const int64_t nb = (a.m + (GEMV_T >> trl) - 1) / (GEMV_T >> trl);
+        xs = nb >= 4 * (int64_t)sm_count(current_device()) * GEMV_MINB;
+    }
+    if (xs && lw >= 4 && !a.y_peers && a.n >= 1024 && a.n <= 12288 && a.n % 4 == 0) {
+        switch (gemv_tr_log2(a.n)) {  // x bulk-copied into shared memory per CTA
+            case 8: return lw == 8 ? gxsm_go<8, 8>(a, s) : gxsm_go<8, 4>(a, s);
+            case 7: return lw == 8 ? gxsm_go<7, 8>(a, s) : gxsm_go<7, 4>(a, s);
+            case 6: return lw == 8 ? gxsm_go<6, 8>(a, s) : gxsm_go<6, 4>(a, s);
+            default: return lw == 8 ? gxsm_go<5, 8>(a, s) : gxsm_go<5, 4>(a, s);
+        }
+    }
     if (gx == 3 && lw >= 4 && gtm_shape_ok(a.n)) {  // TMA ring (gemv_tma.cuh)
         const int nst = gtm_stages(a.n, (size_t)smem_optin(current_device()));
         if (nst >= 2) return a.y_peers ? gtm_trl<true>(a, nst, s) : gtm_trl<false>(a, nst, s);
@@ -556,7 +589,7 @@ lift_status lift_set_variant(lift_variant knob, int value) {
     bool ok = false;
     switch (knob) {
         case LIFT_VAR_LOAD_WIDTH: ok = value == 0 || value == 1 || value == 4 || value == 8; break;
-        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 4; break;
+        case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 5; break;
         case LIFT_VAR_PREFETCH: ok = value >= 0 && value <= 2; break;
         case LIFT_VAR_ORDER: ok = value >= 0 && value <= 2; break;
         default: break;

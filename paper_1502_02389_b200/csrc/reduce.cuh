@@ -45,6 +45,9 @@ namespace lift {
 #ifndef LIFT_RED_RB
 #define LIFT_RED_RB 2
 #endif
+#ifndef LIFT_RED_EXPT
+#define LIFT_RED_EXPT 0  // timing experiments only (never the product)
+#endif
 #ifndef LIFT_RED_TMA
 #define LIFT_RED_TMA 0  // NEXT-4 (tune.py): chunks arrive by TMA bulk copy into shared memory
 #endif
@@ -417,7 +420,14 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
     if (lane == 0) {
         a.chunk_part[c] = pairwise8(wbuf[parity]);
         const int64_t gcount = min((int64_t)RED_G, a.nc - g * RED_G);
+#if LIFT_RED_EXPT == 1  // TIMING EXPERIMENT ONLY (wrong results): no CTA waits for a ticket
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.tick[g]) : "memory");
+        (void)gcount;
+        last = 0;
+        if (c == 0 && lane == 0) *a.out_f32 = 0.f;
+#else
         last = (ticket_acq_rel(&a.tick[g]) == (unsigned)(gcount - 1));
+#endif
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
 

@@ -37,7 +37,8 @@ def run_all(lift, off):
         x = fill(n, 1, gen.TID_X, off=off)
         y = fill(n, 1, gen.TID_Y, off=off)
         out += [bits(lift.scal(3.0, x)), bits(lift.asum(x)), bits(lift.dot(x, y))]
-    for m, n in ((300, 2048), (257, 4096), (64, 8192), (33, 16384), (16, 24576), (7, 1000)):
+    for m, n in ((300, 2048), (257, 4096), (64, 8192), (50, 12288), (33, 16384), (16, 24576),
+                 (7, 1000)):
         A = fill(m * n, 2, gen.TID_A, 0.0, 3.0).view(m, n)
         gx = fill(n, 2, gen.TID_X, 0.0, 1.0)
         gy = fill(m, 2, gen.TID_Y, 0.0, 2.0)
@@ -45,7 +46,7 @@ def run_all(lift, off):
     return out
 
 
-@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3, 4)),
+@pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3, 4, 5)),
                                          ("prefetch", (1, 2)), ("order", (1, 2))])
 @pytest.mark.parametrize("off", [0, 4])
 def test_variants_bit_identical(lift, knob, values, off):
@@ -59,13 +60,13 @@ def test_variants_bit_identical(lift, knob, values, off):
         lift.set_variant(knob, 0)
 
 
-@pytest.mark.parametrize("var", [2, 3, 4])
+@pytest.mark.parametrize("var", [2, 3, 4, 5])
 def test_staged_x_gemv_matches_oracle(lift, var):
     """The gemv x-strategy kernels (LIFT_VAR_GEMV_X = 2: x in shared memory + register ring;
     3: + TMA ring; 4: two rows per thread) against the oracle directly, with a partial last
     row block and signed inputs."""
     lift.set_variant("gemv_x", var)
-    for m, n in ((1001, 8192), (65, 4096), (3, 16384), (37, 2048)):
+    for m, n in ((1001, 8192), (65, 4096), (3, 16384), (37, 2048), (9, 12288)):
         A = gen.host(m * n, 7, gen.TID_A).reshape(m, n)
         x = gen.host(n, 7, gen.TID_X)
         y = gen.host(m, 7, gen.TID_Y)
