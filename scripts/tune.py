@@ -51,8 +51,12 @@ SPACE = {
     # gemv toLocal(x) strategies (RUNTIME knob LIFT_VAR_GEMV_X, same build): x through L1
     # widened per use; x fp64 in shared memory + register ring; x fp64 in shared memory +
     # TMA ring of A row segments (warp-specialised producer)
-    "gemv_x": [("x_l1", "", "gemv_x=1"), ("x_smem_regring", "", "gemv_x=2"),
-               ("x_smem_tmaring", "", "gemv_x=3"), ("x_two_rows", "", "gemv_x=4")],
+    "gemv_x": [("x_l1", "", "gemv_x=1"), ("x_tma_smem", "", "gemv_x=5"),
+               ("x_smem_regring", "", "gemv_x=2"), ("x_smem_tmaring", "", "gemv_x=3"),
+               ("x_two_rows", "", "gemv_x=4")],
+    # TMA L2 prefetch before the PDL wait and the reductions' chunk order (runtime knobs)
+    "prefetch": [("pf_off", "", "prefetch=1"), ("pf_on", "", "prefetch=2")],
+    "order": [("ascending", "", "order=1"), ("descending", "", "order=2")],
 }
 
 
