@@ -1,5 +1,5 @@
 """BASELINE configs[3] (C4: gemv 8192 x 8192 row-sharded) and configs[4] (C5: dot sharded
-with a scalar combine) as two-rank STRONG-scaling runs, checked against the ORACLE.
+with a scalar combine) as 2-, 3- and 4-rank STRONG-scaling runs, checked against the ORACLE.
 
 Only one GPU is available: both ranks run on cuda:0 as two processes with the gloo backend
 (NCCL refuses two ranks on one device), so the 'nccl' X1 path's all-gathers travel through
@@ -78,9 +78,7 @@ def _worker(rank, world, port, q):
         q.put((rank, "error: " + repr(e) + traceback.format_exc()))
 
 
-@pytest.fixture(scope="module")
-def two_rank_results():
-    world = 2
+def _run(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -96,6 +94,11 @@ def two_rank_results():
     for r in range(world):
         assert not isinstance(res[r], str), res[r]
     return res
+
+
+@pytest.fixture(scope="module")
+def two_rank_results():
+    return _run(2)
 
 
 def test_c4_two_ranks_match_oracle_and_unsharded(two_rank_results):
@@ -134,3 +137,35 @@ def test_c5_two_ranks_match_oracle_and_unsharded(two_rank_results):
     dev = torch.device("cuda:0")
     full = lift.dot(torch.from_numpy(xh).to(dev), torch.from_numpy(yh).to(dev))
     assert np.array_equal(full.cpu().numpy().view(np.uint32), res[0]["c5_nccl"])
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_c4_c5_more_ranks(world):
+    """Three (uneven split) and four ranks on the one GPU: gemv rows are independent, so the
+    gathered y equals the unsharded call bit for bit at any split; the dot's combine is the
+    pairwise tree over p partials — bit-identical to the unsharded call when every rank owns
+    a power-of-two number of canonical groups (p = 4: 32 each), within 1e-5 of the oracle
+    otherwise (p = 3: 43 + 43 + 42 groups)."""
+    import paper_1502_02389_b200 as lift
+    res = _run(world)
+    for r in range(world):
+        for yb in res[r]["c4_fused"]:
+            assert np.array_equal(yb, res[0]["c4_nccl"])
+        assert np.array_equal(res[r]["c4_nccl"], res[0]["c4_nccl"])
+        for d in res[r]["c5_fused"]:
+            assert np.array_equal(d, res[0]["c5_nccl"])
+    dev = torch.device("cuda:0")
+    A = gen.host(M * N, 0, gen.TID_A, lo=0.0, hi=3.0).reshape(M, N)
+    x = gen.host(N, 0, gen.TID_X, lo=0.0, hi=1.0)
+    y = gen.host(M, 0, gen.TID_Y, lo=0.0, hi=2.0)
+    full = lift.gemv(torch.from_numpy(A).to(dev), torch.from_numpy(x).to(dev),
+                     torch.from_numpy(y).to(dev), ALPHA, BETA)
+    assert np.array_equal(full.cpu().numpy().view(np.uint32), res[0]["c4_nccl"])
+    xh = gen.host(N5, 0, gen.TID_X, lo=0.0, hi=1.0)
+    yh = gen.host(N5, 0, gen.TID_Y, lo=0.0, hi=2.0)
+    got = float(res[0]["c5_nccl"].view(np.float32)[0])
+    ref = oracle.dot(xh, yh)
+    assert abs(got - ref) <= 1e-5 * abs(ref)
+    if world == 4:
+        fulld = lift.dot(torch.from_numpy(xh).to(dev), torch.from_numpy(yh).to(dev))
+        assert np.array_equal(fulld.cpu().numpy().view(np.uint32), res[0]["c5_nccl"])
