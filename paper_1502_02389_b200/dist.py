@@ -64,7 +64,7 @@ def _world(group):
 def gather_partials(partial: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather one fp64 partial per rank into a rank-ordered [p] tensor."""
     p = _world(group)
-    if p == 1:
+    if not dist.is_initialized():
         return partial.reshape(1)
     out = torch.empty(p, dtype=partial.dtype, device=partial.device)
     if dist.get_backend(group) == "nccl":
@@ -81,7 +81,7 @@ def gather_rows(y_slice: torch.Tensor, m: int, group=None, out: torch.Tensor | N
     p = _world(group)
     if out is None:
         out = torch.empty(m, dtype=y_slice.dtype, device=y_slice.device)
-    if p == 1:
+    if not dist.is_initialized():
         out.copy_(y_slice)
         return out
     rank = dist.get_rank(group)
