@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(RED_T, DotOp<double>::kMinBlocks) gemv_split_k
                 last = (ticket_acq_rel(&tk[g]) == (unsigned)(gcount - 1));
             }
             if (__shfl_sync(0xffffffffu, last, 0)) {
-                ticket_acquired();
+                ticket_acquired(&tk[g]);
                 const int64_t g0 = g * RED_G;
                 const double gv = warp_fold_leaves(cp + g0, min((int64_t)RED_G, s.nc - g0));
                 if (s.ng == 1) {
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(RED_T, DotOp<double>::kMinBlocks) gemv_split_k
                         last = (ticket_acq_rel(&tk[s.ng]) == (unsigned)(s.ng - 1));
                     }
                     if (__shfl_sync(0xffffffffu, last, 0)) {
-                        ticket_acquired();
+                        ticket_acquired(&tk[s.ng]);
                         const double d = warp_fold_leaves(gpart, s.ng);
                         if (lane == 0) {
                             tk[s.ng] = 0u;

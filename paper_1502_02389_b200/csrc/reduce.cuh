@@ -175,19 +175,31 @@ __device__ __forceinline__ void xchg_combine(const ReduceArgs& a, double total) 
 // other lanes' leaf loads after lane 0's acquire.  (LIFT_SC_FENCE: the __threadfence
 // pair instead, for A/B runs.)
 __device__ __forceinline__ unsigned ticket_acq_rel(unsigned* t) {
-#if LIFT_SC_FENCE
+#if LIFT_SC_FENCE == 1
     __threadfence();
     return atomicAdd(t, 1u);
+#elif LIFT_SC_FENCE == 2  // (A/B) release-only ticket; the last CTA acquires separately
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    return old;
 #else
     unsigned old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
     return old;
 #endif
 }
-__device__ __forceinline__ void ticket_acquired() {
-#if LIFT_SC_FENCE
+__device__ __forceinline__ void ticket_acquired(const unsigned* t) {
+#if LIFT_SC_FENCE == 1
+    (void)t;
     __threadfence();
+#elif LIFT_SC_FENCE == 2
+    if ((threadIdx.x & 31) == 0) {  // acquire: synchronizes with every release on the ticket
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(t) : "memory");
+    }
+    __syncwarp();
 #else
+    (void)t;
     __syncwarp();
 #endif
 }
@@ -432,7 +444,7 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
 
     // Last chunk of group g: fold the group's RED_G chunk partials (pairwise).
-    ticket_acquired();
+    ticket_acquired(&a.tick[g]);
     const int64_t g0 = g * RED_G;
     const double gpart = warp_fold_leaves(a.chunk_part + g0, min((int64_t)RED_G, a.nc - g0));
     if (a.ng == 1) {  // one group: the pairwise fold over one leaf is the leaf itself
@@ -454,7 +466,7 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
 
     // Last group: final pairwise fold over the group partials, round once.
-    ticket_acquired();
+    ticket_acquired(&a.tick[a.ng]);
     const double total = warp_fold_leaves(a.group_part, a.ng);
     if (lane == 0) a.tick[a.ng] = 0u;
     if (a.peers) {

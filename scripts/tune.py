@@ -39,7 +39,8 @@ SPACE = {
                   ("s256x2", "-DLIFT_SCAL_T=256 -DLIFT_SCAL_U=2"),
                   ("s256x4", "-DLIFT_SCAL_T=256 -DLIFT_SCAL_U=4")],
     "pdl": [("pdl_on", "-DLIFT_PDL=1"), ("pdl_off", "-DLIFT_PDL=0")],
-    "ticket_fence": [("acq_rel", "-DLIFT_SC_FENCE=0"), ("sc_fence", "-DLIFT_SC_FENCE=1")],
+    "ticket_fence": [("acq_rel", "-DLIFT_SC_FENCE=0"), ("sc_fence", "-DLIFT_SC_FENCE=1"),
+                     ("release_then_acquire", "-DLIFT_SC_FENCE=2")],
     # Fig. 7a/7b axes: the intra-warp tree in shared memory (toLocal +
     # iterate(split-2 reduce), the paper's lowering) vs the shuffle butterfly — same bits
     "tree": [("shuffle", "-DLIFT_TREE=1"), ("smem_tree", "-DLIFT_TREE=2")],
