@@ -42,9 +42,6 @@ namespace lift {
 #ifndef LIFT_GEMV_B
 #define LIFT_GEMV_B 4     // vectors per thread in flight (launch shape only, not the order)
 #endif
-#ifndef LIFT_GEMV_PF_AHEAD
-#define LIFT_GEMV_PF_AHEAD 0
-#endif
 #ifndef LIFT_GEMV_EXPT
 #define LIFT_GEMV_EXPT 0  // timing experiments only (scripts/gpu_r2_gemv.sh); never the product
 #endif
@@ -281,12 +278,6 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
     if (a.prefetch && threadIdx.x < RPB && blockIdx.x < a.nblocks) {  // this CTA's first rows
         const int64_t row = (int64_t)blockIdx.x * RPB + threadIdx.x;
         if (row < a.m) prefetch_l2<4>(a.A + row * a.lda, a.n * 4);
-#if LIFT_GEMV_PF_AHEAD  // (A/B) also the rows of the CTA one resident wave later
-        unsigned nsm;
-        asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-        const int64_t r2 = row + (int64_t)nsm * GEMV_MINB * RPB;
-        if (r2 < a.m) prefetch_l2<4>(a.A + r2 * a.lda, a.n * 4);
-#endif
     }
     pdl_wait();
     pdl_trigger();

@@ -36,9 +36,6 @@
 
 namespace lift {
 
-#ifndef LIFT_GXS_ONESHOT
-#define LIFT_GXS_ONESHOT 0  // 1 (A/B): one block per CTA, hardware-scheduled, no stealing
-#endif
 #ifndef LIFT_GXS_T
 #define LIFT_GXS_T 256   // threads per CTA
 #endif
@@ -117,9 +114,7 @@ __global__ void __launch_bounds__(GXS_T, LIFT_GXS_MINB) gemv_xs_kernel(GemvArgs 
         const int64_t r = b * RP + rsub;
         return a.A + (r < a.m ? r : a.m - 1) * a.lda;  // dead rows re-read a live one
     };
-#if !LIFT_GXS_ONESHOT
     if (t == 0) clc_try_cancel(clc);
-#endif
     const float* rp = row_ptr(blk);
     f8 ring[P];
 #pragma unroll
@@ -137,7 +132,6 @@ __global__ void __launch_bounds__(GXS_T, LIFT_GXS_MINB) gemv_xs_kernel(GemvArgs 
         const int fetch_round = K > P ? P : 0;  // learn the next block one round in
         for (int k0 = 0; k0 < K; k0 += P) {
             const bool last_round = k0 + P == K;
-#if !LIFT_GXS_ONESHOT
             if (k0 == fetch_round) {  // the next block: L2-prefetch its rows now, and its
                 more = clc_fetch(clc, next);  // first ring loads go out before this row's tree
                 if (more) {
@@ -145,7 +139,6 @@ __global__ void __launch_bounds__(GXS_T, LIFT_GXS_MINB) gemv_xs_kernel(GemvArgs 
                     if (tp == 0) prefetch_l2<4>(rpn, a.n * 4);
                 }
             }
-#endif
 #pragma unroll
             for (int j = 0; j < P; ++j) {
                 const f8 av = ring[j];
