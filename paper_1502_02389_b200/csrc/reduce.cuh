@@ -45,6 +45,9 @@ namespace lift {
 #ifndef LIFT_RED_RB
 #define LIFT_RED_RB 2
 #endif
+#ifndef LIFT_RED_FLAT
+#define LIFT_RED_FLAT 1  // one ticket level + whole-CTA fold for 256 < nc <= 2048 (mid sizes)
+#endif
 #ifndef LIFT_RED_EXPT
 #define LIFT_RED_EXPT 0  // timing experiments only (never the product)
 #endif
@@ -423,6 +426,45 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
     }
 #ifdef LIFT_TRACE
     if (t == 0 && c < 65536) g_trace[3 * c + 1] = gtimer();
+#endif
+#if LIFT_RED_FLAT
+    // Mid sizes (256 < nc <= 2048 chunks, one chunk per CTA): ONE ticket level and the whole
+    // last CTA folds every chunk partial — blk = p2(nc)/256 leaves per thread, warp
+    // butterfly, 8 warp values pairwise: the pairwise tree over the chunk partials
+    // zero-padded to p2(nc), i.e. exactly the two-level tree (p2(ceil(nc/256)) * 256 =
+    // p2(nc)), so the same bits with two dependent L2 round trips instead of four.  The
+    // cost: every CTA's warps wait for the ticket at a second CTA barrier.
+    if (a.nc > RED_G && a.nc <= 8 * RED_G && gridDim.x == a.nc && !a.peers) {
+        __shared__ unsigned flat_last;
+        if (t == 0) {
+            a.chunk_part[c] = pairwise8(wbuf[parity]);
+            flat_last = ticket_acq_rel(&a.tick[0]) == (unsigned)(a.nc - 1);
+        }
+        __syncthreads();  // thread 0's acquire (and the verdict) ordered before every thread
+        if (!flat_last) return;
+        int64_t p2 = 1;
+        while (p2 < a.nc) p2 <<= 1;
+        const int blk = (int)(p2 / RED_T);  // 2, 4 or 8
+        double w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t li = (int64_t)t * blk + i;
+            w[i] = (i < blk && li < a.nc) ? __ldcg(a.chunk_part + li) : 0.0;
+        }
+        double v = blk == 2 ? __dadd_rn(w[0], w[1])
+                 : blk == 4 ? __dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3]))
+                            : pairwise8(w);
+        v = warp_pairwise(v);
+        if (lane == 0) wbuf[parity ^ 1][warp] = v;
+        __syncthreads();
+        if (t == 0) {
+            const double total = pairwise8(wbuf[parity ^ 1]);
+            a.tick[0] = 0u;
+            if (a.out_f64) *a.out_f64 = total;
+            if (a.out_f32) *a.out_f32 = __double2float_rn(total);
+        }
+        return;
+    }
 #endif
     if (warp != 0) return;
 
