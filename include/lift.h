@@ -252,6 +252,12 @@ lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float
  *                          reduction after a map over the same vector starts on the tail the
  *                          map left in L2; the fused map+reduce ascending), 1 ascending,
  *                          2 descending
+ *     LIFT_VAR_STAGGER     first-wave stagger (asum/dot/fused map+reduce, gemv): when a launch
+ *                          has more units than resident CTA slots, CTA b of the first wave
+ *                          delays its loads by b x (v ns per 32 KiB it reads), so the wave
+ *                          retires staggered instead of together: 0 auto (2 ns per 32 KiB;
+ *                          for gemv only with x in shared memory), 1 off, 2..64 that many ns
+ *                          per 32 KiB
  *   (The other Fig. 7 axes — shared-memory tree vs shuffle butterfly, TMA bulk loads, chunk
  *   size — are compile-time variants searched by scripts/tune.py.) */
 typedef enum {
@@ -259,7 +265,8 @@ typedef enum {
     LIFT_VAR_GEMV_X = 1,
     LIFT_VAR_PREFETCH = 2,
     LIFT_VAR_ORDER = 3,
-    LIFT_VAR_COUNT = 4
+    LIFT_VAR_STAGGER = 4,
+    LIFT_VAR_COUNT = 5
 } lift_variant;
 lift_status lift_set_variant(lift_variant knob, int value);
 int lift_get_variant(lift_variant knob);

@@ -125,7 +125,7 @@ def set_grid_limit(max_ctas: int) -> None:
 
 
 #: NEXT-4 runtime strategy knobs (lift.h lift_variant); every value gives the same bits.
-VARIANTS = {"load_width": 0, "gemv_x": 1, "prefetch": 2, "order": 3}
+VARIANTS = {"load_width": 0, "gemv_x": 1, "prefetch": 2, "order": 3, "stagger": 4}
 
 
 def set_variant(knob: str, value: int) -> None:

@@ -198,6 +198,25 @@ __device__ __forceinline__ bool in_first_wave(int per_sm) {
     asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
     return blockIdx.x < nsm * (unsigned)per_sm;
 }
+// First-wave stagger.  The CTAs of a launch's first resident wave start together (the PDL
+// wait releases them at once) and issue all their loads at once; with the DRAM queues shared
+// fairly, they then also FINISH together (per-CTA trace, asum 2^24: 888 CTAs end within ~1 us
+// of each other), and the next wave's first loads meet an idle memory pipe for a DRAM
+// latency.  So CTA b < resident of the first wave starts its loads b x ns_per_cta after its
+// own start (lane 0 of every warp spins on %globaltimer; the other lanes wait at the warp
+// barrier): the wave's requests spread over about the time DRAM needs to serve them, its
+// CTAs retire staggered and the next wave streams in behind them.  Timing only: nothing
+// about what is computed depends on it.
+__device__ __forceinline__ void first_wave_stagger(int64_t resident, unsigned ns_per_cta) {
+    if (ns_per_cta && (int64_t)blockIdx.x < resident && blockIdx.x > 0 && (threadIdx.x & 31) == 0) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        const unsigned long long until = t0 + (unsigned long long)blockIdx.x * ns_per_cta;
+        do asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); while (t < until);
+    }
+    __syncwarp();
+}
+
 template <int WHO>
 __device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
 #if LIFT_PREFETCH

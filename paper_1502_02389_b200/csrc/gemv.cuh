@@ -64,6 +64,8 @@ struct GemvArgs {
     float* y_out;
     int64_t nblocks;  // row blocks (of 256/TR rows) of this launch
     int prefetch;     // L2-prefetch each block's rows at CTA start (many waves of blocks)
+    int64_t resident;     // first-wave stagger (common.cuh): CTAs resident at once
+    unsigned stagger_ns;  //   and ns per first-wave CTA index (0: none)
     // NEXT-1 fused all-gather of y (null y_peers: plain local y_out)
     float* const* y_peers;  // p pointers: every rank's full-length y (IPC-mapped)
     int64_t row0;           // global row of local row 0
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(GEMV_T, GEMV_MINB) gemv_kernel(GemvArgs a) {
     }
     pdl_wait();
     pdl_trigger();
+    first_wave_stagger(a.resident, a.stagger_ns);
     constexpr int TR = 1 << TRL;
     constexpr int RP = GEMV_T / TR;  // rows per block
     __shared__ double wv[2][GEMV_T / 32];  // warp values, double-buffered by block parity

@@ -217,11 +217,41 @@ struct XchgArgs {  // NEXT-1: in-kernel cross-GPU combine (all null: single GPU)
 
 // One launch of reduce_kernel (the 128-/256-bit classes; DESC: chunks visited in
 // descending order, reduce.cuh).
+// First-wave stagger (common.cuh first_wave_stagger): LIFT_VAR_STAGGER = 0 auto
+// (LIFT_STAGGER_NS ns per 32 KiB a CTA reads where `auto_on`), 1 off, v >= 2: v ns per
+// 32 KiB.  Applies when every unit has its own CTA and the units outnumber the resident CTA
+// slots.  Measured (scripts/gpu_r2_stagger.sh, 0 / 2 / 3 / 4 / 6 ns): asum 2^24 14.6 -> 13.6,
+// dot 2^24 23.8 -> 22.7, asum 2^28 149.8 -> 148.9, dot 2^26 77.0 -> 76.4, gemv 8192^2 (x in
+// shared memory) 40.6 -> 39.8 us; the gemv x-through-L1 path lost (8192 x 16384 78.2 -> 78.7,
+// 4096^2 14.2 -> 14.3), so auto leaves it off there.
+#ifndef LIFT_STAGGER_NS
+#define LIFT_STAGGER_NS 2
+#endif
+struct Stagger {
+    int64_t resident = 0;
+    unsigned ns = 0;
+};
+inline Stagger stagger_for(int64_t grid, int64_t units, const void* fn, int threads, size_t smem,
+                           int64_t bytes_per_cta, bool auto_on = true) {
+    Stagger st;
+    const int v = var(LIFT_VAR_STAGGER);
+    const int64_t per32k = v == 0 ? (auto_on ? LIFT_STAGGER_NS : 0) : v == 1 ? 0 : v;
+    if (per32k == 0 || grid != units) return st;
+    const int64_t r = (int64_t)sm_count(current_device()) * occupancy(fn, threads, smem);
+    if (r >= units) return st;
+    st.resident = r;
+    st.ns = (unsigned)((per32k * bytes_per_cta + 16384) / 32768);
+    return st;
+}
+
 template <class Op, int LW, int B, bool DESC>
-lift_status reduce_go(const ReduceArgs& a, int64_t nc, cudaStream_t stream) {
+lift_status reduce_go(ReduceArgs a, int64_t nc, cudaStream_t stream) {
     const size_t tsm = (LIFT_RED_TMA && !Op::kMapStore) ? (size_t)RED_C * 4 * (Op::kTwoInputs ? 2 : 1) : 0;
     const void* fn = (const void*)reduce_kernel<Op, LW, B, DESC>;
     const int64_t grid = grid_for(nc, fn, RED_T, tsm, LIFT_PERSISTENT);
+    const Stagger st = stagger_for(grid, nc, fn, RED_T, tsm, (int64_t)RED_C * 4 * (Op::kTwoInputs ? 2 : 1));
+    a.resident = st.resident;
+    a.stagger_ns = st.ns;
     launch(reduce_kernel<Op, LW, B, DESC>, grid, RED_T, tsm, stream, a);
     return launched();
 }
@@ -305,6 +335,9 @@ lift_status reduce_launch(int64_t n, const float* x, const float* y, float* out3
     const size_t tsm = (LIFT_RED_TMA && lw >= 4 && !Op::kMapStore)
                            ? (size_t)RED_C * 4 * (Op::kTwoInputs ? 2 : 1) : 0;
     const int64_t grid = grid_for(L.nc, fn, RED_T, tsm, LIFT_PERSISTENT);
+    const Stagger st = stagger_for(grid, L.nc, fn, RED_T, tsm, (int64_t)RED_C * 4 * (Op::kTwoInputs ? 2 : 1));
+    a.resident = st.resident;
+    a.stagger_ns = st.ns;
     if (lw == 8) launch(reduce_kernel<Op, 8, B>, grid, RED_T, tsm, stream, a);
     else if (lw == 4) launch(reduce_kernel<Op, 4, B>, grid, RED_T, tsm, stream, a);
     else if (lw == 2) launch(reduce_kernel<Op, Op::kMapStore ? 1 : 2, B>, grid, RED_T, 0, stream, a);
@@ -320,8 +353,11 @@ template <int LW, bool ALIAS>
 void scal_go(int64_t grid, int64_t nslots, int head, int tail, float alpha, const float* x,
              float* y, cudaStream_t s) {
     const int pf = var(LIFT_VAR_PREFETCH);
+    constexpr int64_t TILE = (int64_t)SCAL_T * SCAL_U;  // slots per tile
+    const Stagger st = stagger_for(grid, (nslots + TILE - 1) / TILE, (const void*)scal_kernel<LW, ALIAS>,
+                                   SCAL_T, LIFT_SCAL_SMEM, TILE * 64, false);
     launch(scal_kernel<LW, ALIAS>, grid, SCAL_T, LIFT_SCAL_SMEM, s, nslots, head, tail, alpha, x, y,
-           pf == 1 ? 0 : 1);
+           pf == 1 ? 0 : 1, st.resident, st.ns);
 }
 
 template <int LW>
@@ -342,6 +378,9 @@ lift_status gemv_go(GemvArgs a, cudaStream_t s) {
     const int dev = current_device();
     const int pf = var(LIFT_VAR_PREFETCH);
     a.prefetch = pf == 2 || (pf == 0 && a.nblocks >= 4 * (int64_t)sm_count(dev) * occupancy(fn, GEMV_T, 0));
+    const Stagger st = stagger_for(grid, a.nblocks, fn, GEMV_T, 0, rp * a.n * 4, false);
+    a.resident = st.resident;
+    a.stagger_ns = st.ns;
     launch(gemv_kernel<TRL, LW, PEERS>, grid, GEMV_T, 0, s, a);
     return launched();
 }
@@ -356,6 +395,9 @@ lift_status gxsm_go(GemvArgs a, cudaStream_t s) {
     const int pf = var(LIFT_VAR_PREFETCH);
     a.prefetch = pf == 2 || (pf == 0 && a.nblocks >= 4 * (int64_t)sm_count(current_device()) *
                                                          occupancy(fn, GEMV_T, smem));
+    const Stagger st = stagger_for(grid, a.nblocks, fn, GEMV_T, smem, rp * a.n * 4);
+    a.resident = st.resident;
+    a.stagger_ns = st.ns;
     launch(gemv_kernel<TRL, LW, false, true>, grid, GEMV_T, smem, s, a);
     return launched();
 }
@@ -592,6 +634,7 @@ lift_status lift_set_variant(lift_variant knob, int value) {
         case LIFT_VAR_GEMV_X: ok = value >= 0 && value <= 5; break;
         case LIFT_VAR_PREFETCH: ok = value >= 0 && value <= 2; break;
         case LIFT_VAR_ORDER: ok = value >= 0 && value <= 2; break;
+        case LIFT_VAR_STAGGER: ok = value >= 0 && value <= 64; break;
         default: break;
     }
     if (!ok) return LIFT_ERR_INVALID_VALUE;

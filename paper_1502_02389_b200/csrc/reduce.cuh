@@ -135,6 +135,8 @@ struct ReduceArgs {
     unsigned long long epoch;  // > 0, increasing per call on the same buffers
     int* error;                // set to 1 if the peers did not arrive in time
     int prefetch;              // L2-prefetch the CTA's first chunk before the PDL wait
+    int64_t resident;          // first-wave stagger (common.cuh): CTAs resident at once
+    unsigned stagger_ns;       //   and ns per first-wave CTA index (0: none)
 };
 
 // ---- NEXT-1: the outermost reduce across GPUs, inside the kernel -------------------
@@ -462,6 +464,10 @@ __device__ __forceinline__ void chunk_finish(const ReduceArgs& a, int64_t c,
             a.tick[0] = 0u;
             if (a.out_f64) *a.out_f64 = total;
             if (a.out_f32) *a.out_f32 = __double2float_rn(total);
+#ifdef LIFT_TRACE
+            g_trace[3 * 65535] = gtimer();  // timeline marker: the final result store (flat path)
+            g_trace[3 * 65535 + 1] = (unsigned long long)c;
+#endif
         }
         return;
     }
@@ -551,6 +557,7 @@ __global__ void __launch_bounds__(RED_T, LW == 2 ? LIFT_RED_RMINB : Op::kMinBloc
     }
     pdl_wait();
     pdl_trigger();
+    first_wave_stagger(a.resident, a.stagger_ns);  // common.cuh
     __shared__ double wbuf[2][RED_T / 32];  // double-buffered by chunk parity
     constexpr bool kTma = LIFT_RED_TMA && LW >= 4 && !Op::kMapStore;
     __shared__ uint64_t tma_bar;

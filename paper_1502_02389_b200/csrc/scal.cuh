@@ -45,7 +45,8 @@ __device__ __forceinline__ f8 scal_load(const float* p) {
 template <int LW, bool ALIAS>
 __global__ void __launch_bounds__(SCAL_T) scal_kernel(int64_t nslots, int head, int tail,
                                                       float alpha, const float* x, float* y,
-                                                      int prefetch) {
+                                                      int prefetch, int64_t resident = 0,
+                                                      unsigned stagger_ns = 0) {
     // the first wave's tiles, L2-prefetched before the wait (common.cuh prefetch_l2)
     if (prefetch && threadIdx.x == 0 && in_first_wave(2048 / SCAL_T)) {
         const int64_t s0 = (int64_t)blockIdx.x * SCAL_T * SCAL_U;
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(SCAL_T) scal_kernel(int64_t nslots, int head, 
     }
     pdl_wait();
     pdl_trigger();
+    first_wave_stagger(resident, stagger_ns);  // common.cuh
     const int t = threadIdx.x;
     if (blockIdx.x == 0) {
         if (t < head) y[t] = alpha * x[t];

@@ -11,6 +11,8 @@ import torch  # noqa: E402
 
 import lift_inputs as gen  # noqa: E402
 import paper_1502_02389_b200 as lift  # noqa: E402
+for _kv in filter(None, os.environ.get("LIFT_SET_VARIANTS", "").split(",")):
+    lift.set_variant(_kv.split("=")[0], int(_kv.split("=")[1]))  # NEXT-4 runtime knobs
 
 dev = torch.device("cuda:0")
 X = gen.fill_device(torch.empty(1 << 28, device=dev), 0, gen.TID_X, 0, 0, -1.0, 1.0)

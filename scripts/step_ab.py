@@ -17,6 +17,8 @@ import torch  # noqa: E402
 
 import lift_inputs as gen  # noqa: E402
 import paper_1502_02389_b200 as lift  # noqa: E402
+for _kv in filter(None, os.environ.get("LIFT_SET_VARIANTS", "").split(",")):
+    lift.set_variant(_kv.split("=")[0], int(_kv.split("=")[1]))  # NEXT-4 runtime knobs
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 dev = torch.device("cuda:0")

@@ -54,4 +54,7 @@ out = {"n": n, "op": op, "event_us": e0.elapsed_time(e1) * 1e3, "chunks": nc,
        "sms_used": int(len(np.unique(sm))),
        "start_quantiles_us": [float(np.percentile(start, q)) for q in (1, 10, 50, 90, 99)],
        "end_quantiles_us": [float(np.percentile(end, q)) for q in (1, 10, 50, 90, 99)]}
-print(json.dumps(out, indent=1))
+bins = np.arange(0, float(end.max()) + 0.5, 0.5)
+out["starts_per_0.5us"] = np.histogram(start, bins)[0].tolist()
+out["ends_per_0.5us"] = np.histogram(end, bins)[0].tolist()
+print(json.dumps(out))

@@ -187,6 +187,7 @@ def test_variant_api_host_only():
     assert lib.lift_set_variant(1, 7) == INVALID   # gemv x strategy 7
     assert lib.lift_set_variant(9, 0) == INVALID   # no such knob
     assert lib.lift_get_variant(9) == -1
-    for knob, v in ((0, 4), (0, 1), (1, 2)):
+    assert lib.lift_set_variant(4, 65) == INVALID  # stagger beyond 64 ns per 32 KiB
+    for knob, v in ((0, 4), (0, 1), (1, 2), (4, 1), (4, 7)):
         assert lib.lift_set_variant(knob, v) == OK and lib.lift_get_variant(knob) == v
         assert lib.lift_set_variant(knob, 0) == OK and lib.lift_get_variant(knob) == 0

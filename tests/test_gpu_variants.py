@@ -33,12 +33,12 @@ def fill(n, seed, tid, lo=-1.0, hi=1.0, off=0):
 
 def run_all(lift, off):
     out = []
-    for n in (1, 9, 8191, 8192 * 3 + 5, 1 << 20):
+    for n in (1, 9, 8191, 8192 * 3 + 5, 1 << 20, (1 << 23) + 13):  # the last: > one resident wave
         x = fill(n, 1, gen.TID_X, off=off)
         y = fill(n, 1, gen.TID_Y, off=off)
         out += [bits(lift.scal(3.0, x)), bits(lift.asum(x)), bits(lift.dot(x, y))]
     for m, n in ((300, 2048), (257, 4096), (64, 8192), (50, 12288), (33, 16384), (16, 24576),
-                 (7, 1000)):
+                 (7, 1000), (8200, 2048)):  # the last: more row blocks than resident CTAs
         A = fill(m * n, 2, gen.TID_A, 0.0, 3.0).view(m, n)
         gx = fill(n, 2, gen.TID_X, 0.0, 1.0)
         gy = fill(m, 2, gen.TID_Y, 0.0, 2.0)
@@ -47,7 +47,8 @@ def run_all(lift, off):
 
 
 @pytest.mark.parametrize("knob,values", [("load_width", (1, 4, 8)), ("gemv_x", (1, 2, 3, 4, 5)),
-                                         ("prefetch", (1, 2)), ("order", (1, 2))])
+                                         ("prefetch", (1, 2)), ("order", (1, 2)),
+                                         ("stagger", (1, 2, 8))])
 @pytest.mark.parametrize("off", [0, 4])
 def test_variants_bit_identical(lift, knob, values, off):
     ref = run_all(lift, off)
