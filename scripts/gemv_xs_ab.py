@@ -23,6 +23,8 @@ def child(reps=24):
     import lift_inputs as gen
     import paper_1502_02389_b200 as lift
     dev = torch.device("cuda:0")
+    for kv in filter(None, os.environ.get("LIFT_SET_VARIANTS", "").split(",")):
+        lift.set_variant(kv.split("=")[0], int(kv.split("=")[1]))  # other knobs, fixed
     shapes = SHAPES
     if os.environ.get("AB_SHAPES"):
         shapes = [tuple(int(v) for v in s.split("x")) for s in os.environ["AB_SHAPES"].split(",")]
