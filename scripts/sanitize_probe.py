@@ -61,5 +61,14 @@ lift.set_variant("load_width", 4)
 x, y = rnd(C + 77), rnd(C + 77)
 lift.scal(3.0, x), lift.dot(x, y)
 lift.set_variant("load_width", 0)
+# launches with more units than resident CTAs: the first-wave stagger (default on for the
+# reductions and the x-in-shared-memory gemv; 4 = also scal and the x-through-L1 gemv)
+for st in (0, 4):
+    lift.set_variant("stagger", st)
+    x, y = rnd((1 << 23) + 13), rnd((1 << 23) + 13)
+    lift.asum(x), lift.dot(x, y), lift.scal(3.0, x), lift.scal_asum(2.0, x)
+    A = torch.rand(4100, 2048, generator=g).to(dev)
+    lift.gemv(A, rnd(2048), rnd(4100), 1.5, 0.5)
+lift.set_variant("stagger", 0)
 torch.cuda.synchronize()
 print("sanitize probe ok")

@@ -58,6 +58,9 @@ SPACE = {
     # TMA L2 prefetch before the PDL wait and the reductions' chunk order (runtime knobs)
     "prefetch": [("pf_off", "", "prefetch=1"), ("pf_on", "", "prefetch=2")],
     "order": [("ascending", "", "order=1"), ("descending", "", "order=2")],
+    # first-wave stagger, ns per 32 KiB a CTA reads (runtime knob LIFT_VAR_STAGGER; default 2)
+    "stagger": [("stagger_off", "", "stagger=1"), ("stagger_3ns", "", "stagger=3"),
+                ("stagger_4ns", "", "stagger=4"), ("stagger_6ns", "", "stagger=6")],
 }
 
 
