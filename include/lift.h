@@ -96,6 +96,14 @@ const char* lift_last_cuda_error(void);
  * reductions 2-20%, and is not part of the product.) */
 size_t lift_workspace_bytes(int64_t n);
 
+/* Host-side check of that contract, off the hot path: waits for `stream`, copies the
+ *   workspace's ticket region (its last bytes, a function of ws_bytes only) to the host and
+ *   returns LIFT_OK if every ticket is zero, LIFT_ERR_WORKSPACE if any is not (a call was
+ *   aborted, two calls overlapped on the buffer, or it was never zero-filled — zero-fill it
+ *   again before the next call), LIFT_ERR_CUDA if the copy fails.  ws_bytes as passed to the
+ *   reductions; ws must be 16-byte aligned (else LIFT_ERR_INVALID_VALUE). */
+lift_status lift_workspace_check(const void* ws, size_t ws_bytes, lift_stream_t stream);
+
 /* S1 — scal: y[i] = RN_fp32(alpha * x[i]) for 0 <= i < n.
  *   x: n floats in; y: n floats out; y == x (in place) is allowed, any other overlap
  *   is undefined.  n == 0 launches nothing.  Bit-exact by construction. */

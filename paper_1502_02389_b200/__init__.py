@@ -100,8 +100,20 @@ class Workspace:
         return self.buf.data_ptr()
 
     def reset(self) -> None:
-        """Zero-fill again (clears the tickets and the sticky error word)."""
+        """Zero-fill again (clears the tickets)."""
         self.buf.zero_()
+
+    def check(self) -> bool:
+        """lift_workspace_check: True if every last-block-done ticket is zero (the contract
+        holds); False if a call was aborted or overlapped on this buffer (then reset()).
+        Synchronises with the current stream; off the hot path."""
+        dev = self.buf.device
+        with _on(dev):
+            st = lib.lift_workspace_check(self.ptr, self.nbytes, _stream_handle(dev))
+        if st == 3:  # LIFT_ERR_WORKSPACE
+            return False
+        check(st)
+        return True
 
 
 _ws_lock = threading.Lock()

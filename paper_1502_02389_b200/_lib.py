@@ -20,7 +20,7 @@ EXPORTS = (
     "lift_xchg_create", "lift_xchg_destroy", "lift_ipc_get_handle", "lift_ipc_open_handle",
     "lift_ipc_close_handle", "lift_asum_allreduce", "lift_dot_allreduce", "lift_ipc_alloc",
     "lift_gemv_allgather", "lift_gemv_ws", "lift_gemv_workspace_bytes", "lift_set_variant",
-    "lift_get_variant", "lift_last_cuda_error",
+    "lift_get_variant", "lift_last_cuda_error", "lift_workspace_check",
 )
 
 LIFT_OK = 0
@@ -40,6 +40,7 @@ def _load():
         "lift_abi_version": ([], _int),
         "lift_status_string": ([_int], ctypes.c_char_p),
         "lift_workspace_bytes": ([_i64], _sz),
+        "lift_workspace_check": ([_vp, _sz, _vp], _int),
         "lift_scal": ([_i64, _f32, _vp, _vp, _vp], _int),
         "lift_asum": ([_i64, _vp, _vp, _vp, _sz, _vp], _int),
         "lift_dot": ([_i64, _vp, _vp, _vp, _vp, _sz, _vp], _int),

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/lift.h"
 #include "canon.h"
@@ -625,6 +626,26 @@ const char* lift_last_cuda_error(void) {
 }
 
 size_t lift_workspace_bytes(int64_t n) { return ws_bytes_for(n < 0 ? 0 : n); }
+
+lift_status lift_workspace_check(const void* ws, size_t ws_bytes, lift_stream_t stream) {
+    if (!ws) return LIFT_ERR_NULL_POINTER;
+    if (reinterpret_cast<uintptr_t>(ws) & 15) return LIFT_ERR_INVALID_VALUE;
+    const size_t wf = ws_bytes & ~(size_t)15;
+    const size_t r = ticket_region(wf);
+    if (wf < r) return LIFT_ERR_WORKSPACE;
+    std::vector<unsigned> h(r / 4);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(h.data(), static_cast<const char*>(ws) + (wf - r), r,
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        g_last_cuda = e;
+        return LIFT_ERR_CUDA;
+    }
+    for (unsigned v : h)
+        if (v) return LIFT_ERR_WORKSPACE;
+    return LIFT_OK;
+}
 
 lift_status lift_set_variant(lift_variant knob, int value) {
     if ((int)knob < 0 || (int)knob >= LIFT_VAR_COUNT) return LIFT_ERR_INVALID_VALUE;

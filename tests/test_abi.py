@@ -85,6 +85,9 @@ def C_ELEMS():
 def test_argument_errors_are_synchronous():
     from paper_1502_02389_b200._lib import lib
     p = 4096  # a fake, aligned, never-dereferenced address
+    assert lib.lift_workspace_check(None, 4096, None) == NULLP
+    assert lib.lift_workspace_check(p + 4, 4096, None) == INVALID  # not 16-byte aligned
+    assert lib.lift_workspace_check(p, 0, None) == WS               # no room for tickets
     assert lib.lift_scal(-1, 1.0, p, p, None) == INVALID
     assert lib.lift_scal(0, 1.0, None, None, None) == OK          # empty: nothing launched
     assert lib.lift_scal(5, 1.0, None, p, None) == NULLP

@@ -564,7 +564,14 @@ def test_workspace_reset_restores_the_contract(lift):
     wf = ws.nbytes & ~15
     region = ((wf // 512 + 2) * 4 + 15) & ~15
     t0 = wf - region
+    assert ws.check()  # lift_workspace_check: every ticket zero after complete calls
     ws.buf[t0:t0 + 4].view(torch.int32).fill_(5)
+    assert not ws.check()  # the broken contract is detected on the host
     lift.asum(x, ws=ws)
     ws.reset()
+    assert ws.check()
     assert lift.asum(x, ws=ws).item() == good
+    for k in (1, region // 4 - 1):  # any ticket of the region, not only the first
+        ws.buf[t0 + 4 * k:t0 + 4 * k + 4].view(torch.int32).fill_(1)
+        assert not ws.check()
+        ws.reset()
