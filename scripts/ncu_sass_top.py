@@ -1,6 +1,7 @@
 """Top SASS instructions by warp-stall samples from an ncu report (--import-source, -lineinfo):
-    python scripts/ncu_sass_top.py report.ncu-rep [N] [--all]
---all prints every instruction in address order with its samples (for reading the loop)."""
+    python scripts/ncu_sass_top.py report.ncu-rep [N] [--all] [--kernel REGEX]
+--all prints every instruction in address order with its samples (for reading the loop);
+--kernel picks the kernel of a multi-kernel report (ncu -k regex:REGEX)."""
 import csv
 import io
 import subprocess
@@ -8,9 +9,15 @@ import sys
 
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kf = []
+if "--kernel" in sys.argv:
+    kf = ["-k", "regex:" + sys.argv[sys.argv.index("--kernel") + 1]]
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
+nxt = [i for i, l in enumerate(lines) if i > 0 and l.startswith('"Kernel Name"')]
+if nxt:  # the page may list a kernel more than once: keep the first block
+    lines = lines[:nxt[0]]
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
 h = rows[0]
 ia, isrc, iss = h.index("Address"), h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
