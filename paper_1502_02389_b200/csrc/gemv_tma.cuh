@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(GTM_T, 1) gemv_tma_kernel(GemvArgs a, int nst)
         mbar_init(clc_bar, 1);
         for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], GTM_CW);
+            mbar_init(&empty[s], GTM_CT);  // every consumer thread releases the stage
         }
     }
     pdl_wait();  // x, A, y may be the previous kernel's output
@@ -180,8 +180,10 @@ __global__ void __launch_bounds__(GTM_T, 1) gemv_tma_kernel(GemvArgs a, int nst)
                     acc[r][2 * jj + 1] = __fma_rn((double)av[2 * jj + 1], xv[jj].y, acc[r][2 * jj + 1]);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            // each consumer thread releases the stage after its own reads of it (the arrive
+            // orders them before the producer's next bulk copy into the stage; one arrive per
+            // warp after __syncwarp was equivalent but not visible to compute-sanitizer racecheck)
+            mbar_arrive(&empty[s]);
             if (++s == nst) {
                 s = 0;
                 ph ^= 1u;
