@@ -111,7 +111,8 @@ def time_b2b(fn, nbytes, reps=50):
 
 out = {"note": "device time per launch, CUDA graph replay, L2 flushed before each launch, "
                "median of 20 (p10/p90; us_diff = graph-difference timing, see time_op); "
-               "*_b2b: L2-warm back-to-back graph replays; HBM roofline denominators: 6451.8 GB/s measured, 8 TB/s nominal"}
+               "*_b2b: L2-warm back-to-back graph replays; HBM roofline denominators: "
+               f"{PEAK} GB/s measured (frac_measured), 8 TB/s nominal (frac_8TBs)"}
 # floor: a one-element torch fill, timed the same way (launch + one tiny CTA after a flush)
 r0 = torch.empty(1, dtype=torch.float32, device=dev)
 out["null_fill_1"] = time_op(lambda: r0.fill_(0.0), 4)
