@@ -75,3 +75,30 @@ def test_staged_x_gemv_matches_oracle(lift, var):
                         torch.from_numpy(y).to(DEV), -1.25, 0.75).cpu().numpy().astype(np.float64)
         ref = oracle.gemv(A, x, y, -1.25, 0.75)
         assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (m, n)
+
+
+def test_stagger_full_size_bit_identical(lift):
+    """The first-wave stagger (on by default for the reductions and the x-in-shared-memory
+    gemv) at BASELINE's full sizes and in its launch configuration: asum 2^28, dot 2^26, the
+    fused scal+asum 2^28 and gemv 8192^2 give the same bits with the stagger off, on (default)
+    and wide (16 ns per 32 KiB), and scal (stagger only when forced) the same bytes."""
+    n, nd, m = 1 << 28, 1 << 26, 8192
+    x = fill(n, 5, gen.TID_X)
+    y = fill(nd, 5, gen.TID_Y)
+    A = fill(m * m, 5, gen.TID_A, 0.0, 3.0).view(m, m)
+    gx = fill(m, 5, gen.TID_X, 0.0, 1.0)
+    gy = fill(m, 5, gen.TID_Y, 0.0, 2.0)
+
+    def run():
+        _, r = lift.scal_asum(2.0, x[:nd])
+        return [bits(lift.asum(x)), bits(lift.dot(x[:nd], y)), bits(r),
+                bits(lift.gemv(A, gx, gy, 1.5, 0.5)),
+                bits(lift.scal(3.0, x[:nd]))]
+
+    ref = run()
+    for v in (1, 16):
+        lift.set_variant("stagger", v)
+        got = run()
+        for i, (a, b) in enumerate(zip(ref, got)):
+            assert np.array_equal(a, b), (v, i)
+    lift.set_variant("stagger", 0)
