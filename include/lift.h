@@ -22,14 +22,18 @@
  *    kernel (none for empty work; a cudaMemsetAsync for an empty reduction) and
  *    returns.  It never synchronises, never allocates and never touches host copies of
  *    the data.  The exceptions are the one-time setup calls of the NEXT-1 exchange
- *    (lift_xchg_create/destroy, lift_ipc_*), which allocate, map or free synchronously.  Results are stream-ordered in device
+ *    (lift_xchg_create/destroy, lift_ipc_*), which allocate, map or free synchronously,
+ *    and the off-hot-path check lift_workspace_check, which waits for its stream.
+ *    Results are stream-ordered in device
  *    memory; read them after your own sync.  A reduction's result is a 1-element
  *    device array, following the paper's "primitives are arrays of length 1"
  *     and reduce's type T[] -> T[1].
  *  - The caller owns every buffer, including the workspace and the exchange buffers
  *    (which lift_xchg_create allocates on the caller's behalf).  The library keeps no
  *    device memory and no mutable state except a per-device cache of the SM count
- *    and kernel occupancies (and the test hook lift_debug_set_grid_limit).
+ *    and kernel occupancies, the process-global NEXT-4 strategy knobs
+ *    (lift_set_variant; none changes a result bit) and the test hook
+ *    lift_debug_set_grid_limit.
  *  - Errors are returned synchronously and nothing is launched:
  *      LIFT_ERR_INVALID_VALUE  n, m < 0; lda < max(1, n); p < 1; a pointer that is
  *                              not 4-byte aligned;
