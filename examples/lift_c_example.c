@@ -52,6 +52,7 @@ int main(void) {
     CHECK(lift_scal(n, 2.0f, x, y, NULL));
     CHECK(lift_dot(n, x, y, res + 1, ws, wsb, NULL));
     CHECK(lift_gemv(m, k, 1.5f, A, k, v, 0.5f, w, wo, NULL));
+    CHECK(lift_workspace_check(ws, wsb, NULL));  /* the tickets are back at zero */
     float hr[2], hwo[3];
     cudaMemcpy(hr, res, 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(hwo, wo, 12, cudaMemcpyDeviceToHost);
