@@ -401,6 +401,20 @@ def test_full_gemv_8192(lift):
     assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref))
 
 
+@pytest.mark.parametrize("m,n", [(4096, 4096), (8192, 16384)])
+def test_full_gemv_paper_sizes(lift, m, n):
+    """The paper's own gemv inputs (reading R12): 4096^2 and 8192 x 16384 (the
+    x-through-L1 path), every element against the oracle at plain relative 1e-6."""
+    A = dev_gen(m * n, 1, gen.TID_A, 0.0, 3.0).view(m, n)
+    x = dev_gen(n, 1, gen.TID_X, 0.0, 1.0)
+    y = dev_gen(m, 1, gen.TID_Y, 0.0, 2.0)
+    got = lift.gemv(A, x, y, 1.5, 0.5).cpu().numpy()
+    ref = oracle.gemv(gen.host(m * n, 1, gen.TID_A, lo=0.0, hi=3.0).reshape(m, n),
+                      gen.host(n, 1, gen.TID_X, lo=0.0, hi=1.0),
+                      gen.host(m, 1, gen.TID_Y, lo=0.0, hi=2.0), 1.5, 0.5)
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref))
+
+
 def test_full_dot_2p31(lift):
     """C5 at full size on one GPU (16 GiB of inputs); the oracle streams the same
     seeded values from the host generator block by block."""
