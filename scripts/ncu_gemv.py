@@ -16,6 +16,8 @@ A = gen.fill_device(torch.empty(m * n, device=dev), 0, gen.TID_A, 0, 0, 0.0, 3.0
 x = gen.fill_device(torch.empty(n, device=dev), 0, gen.TID_X, 0, 0, 0.0, 1.0)
 y = gen.fill_device(torch.empty(m, device=dev), 0, gen.TID_Y, 0, 0, 0.0, 2.0)
 o = torch.empty(m, device=dev)
+if os.environ.get("LIFT_PF"):  # LIFT_VAR_PREFETCH: 1 off, 2 on
+    lift.set_variant("prefetch", int(os.environ["LIFT_PF"]))
 if os.environ.get("GEMV_X"):  # LIFT_VAR_GEMV_X: 1 = x via L1, 2 = x staged fp64 in smem
     lift.set_variant("gemv_x", int(os.environ["GEMV_X"]))
 for _ in range(3):
