@@ -672,9 +672,25 @@ def baseline_configs(lift, gen, torch, dev, x_v, y_v, x_d, y_d, A, g_x, g_y, g_o
     out["C3 scal 2^28"] = timed(lambda: lift.scal(ALPHA_SCAL, x_v, out=y_v), 8 << 28)
     out["C3 asum 2^28"] = timed(lambda: lift.asum(x_v, out=r, ws=ws), 4 << 28)
     m, n = A.shape
-    out["C4 gemv 8192x8192 (p=1)"] = timed(lambda: lift.gemv(A, g_x, g_y, ALPHA, BETA, out=g_out),
-                                           4 * (m * n + n + 2 * m))
+    # C4: rotates over 3 copies of A (> 2x L2), like C2 2^24 over disjoint slices, so every
+    # launch streams its matrix from HBM (scripts/ab.py / tune.py measure the same way)
+    As = [A] + [A.clone() for _ in range(2)]
+    k4 = [0]
+
+    def gemv_rot():
+        i = k4[0] % len(As)
+        k4[0] += 1
+        lift.gemv(As[i], g_x, g_y, ALPHA, BETA, out=g_out)
+    out["C4 gemv 8192x8192 (p=1)"] = timed(gemv_rot, 4 * (m * n + n + 2 * m))
+    del As
     sh = m // 8
+    ks = [0]
+
+    def shard_rot():  # the 8 disjoint p=8 row blocks in turn (268 MB > L2): from HBM
+        i = ks[0] % 8
+        ks[0] += 1
+        lift.gemv(A[i * sh:(i + 1) * sh], g_x, g_y[:sh], ALPHA, BETA, out=g_out[:sh])
+    out["C4 gemv 1024x8192 (one p=8 shard, from HBM)"] = timed(shard_rot, 4 * (sh * n + n + 2 * sh))
     out["C4 gemv 1024x8192 (one p=8 shard, L2-warm)"] = timed(
         lambda: lift.gemv(A[:sh], g_x, g_y[:sh], ALPHA, BETA, out=g_out[:sh]), 4 * (sh * n + n + 2 * sh))
     # C5: dot over 2^31 elements (16 GiB of inputs) on this one GPU, if memory allows
