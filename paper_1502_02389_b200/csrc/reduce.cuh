@@ -39,6 +39,12 @@
 
 namespace lift {
 
+#ifndef LIFT_DOT_MINB
+#define LIFT_DOT_MINB 4  // resident CTAs per SM the dot kernel is compiled for (registers)
+#endif
+#ifndef LIFT_ASUM_MINB
+#define LIFT_ASUM_MINB 6  // the same for asum
+#endif
 #ifndef LIFT_RED_RMINB
 #define LIFT_RED_RMINB 4  // resident CTAs per SM for the realigned (LW 2) reductions
 #endif
@@ -76,7 +82,7 @@ struct AsumOp {
     using rebind = AsumOp<A2>;
     static constexpr bool kTwoInputs = false;
     static constexpr bool kMapStore = false;
-    static constexpr int kMinBlocks = 6;
+    static constexpr int kMinBlocks = LIFT_ASUM_MINB;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float) {
         if constexpr (sizeof(Acc) == 8) return __dadd_rn(acc, fabs((double)a));
         else return __fadd_rn(acc, fabsf(a));  // abs then add, fused
@@ -89,7 +95,7 @@ struct DotOp {
     using rebind = DotOp<A2>;
     static constexpr bool kTwoInputs = true;
     static constexpr bool kMapStore = false;
-    static constexpr int kMinBlocks = 4;
+    static constexpr int kMinBlocks = LIFT_DOT_MINB;
     __device__ __forceinline__ static Acc step(Acc acc, float a, float b) {
         if constexpr (sizeof(Acc) == 8) return __fma_rn((double)a, (double)b, acc);  // exact product
         else return __fmaf_rn(a, b, acc);  // mult then add, one rounding
