@@ -301,7 +301,11 @@ def run_lift(args):
     # X1 for asum/dot at N > 1: the combine fused into the reduction kernel (NEXT-1,
     # peer-memory exchange); LIFT_X1=nccl selects all-gather + lift_combine instead.
     x1_mode = os.environ.get("LIFT_X1", "fused") if world > 1 else "none"
-    xchg = ldist.PeerExchange(group, device=dev) if x1_mode == "fused" else None
+    xchg, x1_note = None, ""
+    if x1_mode == "fused":
+        xchg, x1_note = fused_exchange_or_none(lift, ldist, torch, dist, group, dev)
+        if xchg is None:  # every rank falls back together (agreed below): the NCCL X1 path
+            x1_mode = "nccl"
 
     def x_asum(x, out, ws):
         return xchg.asum(x, out=out, ws=ws) if xchg else ldist.sharded_asum(x, group, out=out, ws=ws)
@@ -482,7 +486,8 @@ def run_lift(args):
                        "x1": {"none": "single GPU", "fused": "asum/dot combine and the gemv y "
                               "all-gather fused into the kernels over peer memory (no NCCL "
                               "launch in the step)",
-                              "nccl": "all-gather + lift_combine; gemv y all-gather"}[x1_mode],
+                              "nccl": "all-gather + lift_combine; gemv y all-gather"}[x1_mode]
+                             + (f" [{x1_note}]" if x1_note else ""),
                        "l2": "no flush: every operand >= 256 MiB > 126 MB L2",
                        "frac_of_8TBs": round(value / world / NOMINAL_HBM, 4)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1),
@@ -509,6 +514,35 @@ def run_lift(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def fused_exchange_or_none(lift, ldist, torch, dist, group, dev):
+    """The NEXT-1 peer-memory exchange, probed end to end once (a fused asum over one chunk
+    per rank, its error word checked); all ranks agree (all-reduce MIN) so that a node where
+    CUDA IPC / P2P does not work falls back to the NCCL X1 path on every rank instead of
+    failing the run.  Returns (PeerExchange or None, note)."""
+    ex, note = None, ""
+    try:
+        ex = ldist.PeerExchange(group, device=dev)
+        if os.environ.get("LIFT_X1_PROBE_FAIL") == str(dist.get_rank(group)):
+            raise RuntimeError("LIFT_X1_PROBE_FAIL test hook")  # exercises the fallback
+        probe = torch.ones(lift.CHUNK_ELEMS, dtype=torch.float32, device=dev)
+        r = ex.asum(probe)
+        torch.cuda.synchronize(dev)
+        ex.check()
+        if float(r.item()) != float(lift.CHUNK_ELEMS * dist.get_world_size(group)):
+            raise RuntimeError(f"probe asum {float(r.item())}")
+    except Exception as e:  # noqa: BLE001 — any failure selects the NCCL path
+        note = f"fused exchange unavailable ({type(e).__name__}: {str(e)[:160]}); NCCL X1 path"
+        ex = None
+    ok = torch.tensor([1 if ex is not None else 0], dtype=torch.int32,
+                      device=dev if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if int(ok.item()) == 0 and ex is not None:
+        ex.close()
+        ex = None
+        note = note or "fused exchange unavailable on another rank; NCCL X1 path"
+    return ex, note
 
 
 def scaling_configs(args, lift, ldist, gen, torch, dist, world, rank, dev, group,
@@ -545,7 +579,8 @@ def scaling_configs(args, lift, ldist, gen, torch, dist, world, rank, dev, group
         return gen.fill_device(torch.empty(n, dtype=torch.float32, device=dev), 0, tid, i0,
                                gen.DIST_UNIFORM, lo, hi)
 
-    ex = xchg if xchg is not None else ldist.PeerExchange(group, device=dev)
+    ex, ex_note = (xchg, "") if xchg is not None else fused_exchange_or_none(
+        lift, ldist, torch, dist, group, dev)
     out = {"note": "strong scaling: fixed global problem split over N ranks; kernel = local "
                    "launch only, fused / nccl = end to end including the X1 exchange; "
                    "median of 5 x %d calls, max over ranks" % reps}
@@ -558,8 +593,8 @@ def scaling_configs(args, lift, ldist, gen, torch, dist, world, rank, dev, group
     go = torch.empty(r1 - r0, device=dev)
     gfull = torch.empty(M, device=dev)
     t_k = timed(lambda: lift.gemv(A, gx, gy, ALPHA, BETA, out=go))
-    t_f = timed(lambda: ex.gemv(A, gx, gy, ALPHA, BETA, M, r0))
-    yf = ex.gemv(A, gx, gy, ALPHA, BETA, M, r0).clone()
+    t_f = timed(lambda: ex.gemv(A, gx, gy, ALPHA, BETA, M, r0)) if ex else None
+    yf = ex.gemv(A, gx, gy, ALPHA, BETA, M, r0).clone() if ex else None
     t_n = timed(lambda: ldist.sharded_gemv(A, gx, gy, ALPHA, BETA, M, group, out_full=gfull,
                                            out_slice=go))
     yn = ldist.sharded_gemv(A, gx, gy, ALPHA, BETA, M, group, out_full=gfull, out_slice=go).clone()
@@ -574,17 +609,22 @@ def scaling_configs(args, lift, ldist, gen, torch, dist, world, rank, dev, group
     barrier()
     bytes_all = 4 * (M * N + world * N + 2 * M)
     c4 = {"rows_per_rank": r1 - r0}
+    paths = ("kernel", "fused", "nccl") if ex else ("kernel", "nccl")
+    if not ex:
+        c4["fused"] = {"unavailable": ex_note}
     for k, t in (("kernel", t_k), ("fused", t_f), ("nccl", t_n)):
+        if t is None:
+            continue
         c4[k] = {"ms": round(t, 4), "GB/s": round(bytes_all / (t * 1e-3) / 1e9, 1),
                  "elements_per_s": float(f"{M * N / (t * 1e-3):.4g}"),
                  "frac_of_8TBs_per_gpu": round(bytes_all / (t * 1e-3) / 1e9 / world / NOMINAL_HBM, 4)}
     if rank == 0:
         c4["t1_ms"] = round(ref["t1"], 4)
-        for k in ("kernel", "fused", "nccl"):
+        for k in paths:
             c4[k]["efficiency_vs_1"] = round(ref["t1"] / (world * c4[k]["ms"]), 4)
-        c4["bits_equal_unsharded"] = bool(torch.equal(yf.view(torch.int32), ref["bits"].view(torch.int32))
-                                          and torch.equal(yn.view(torch.int32),
-                                                          ref["bits"].view(torch.int32)))
+        c4["bits_equal_unsharded"] = bool(
+            (yf is None or torch.equal(yf.view(torch.int32), ref["bits"].view(torch.int32)))
+            and torch.equal(yn.view(torch.int32), ref["bits"].view(torch.int32)))
     out["C4 gemv 8192x8192 row-sharded"] = c4
     del A
 
@@ -596,8 +636,8 @@ def scaling_configs(args, lift, ldist, gen, torch, dist, world, rank, dev, group
     r = torch.empty(1, device=dev)
     p64 = torch.empty(1, dtype=torch.float64, device=dev)
     t_k = timed(lambda: lift.dot_partial(x, y, out=p64, ws=ws), nreps=3)
-    t_f = timed(lambda: ex.dot(x, y, out=r, ws=ws), nreps=3)
-    rf = ex.dot(x, y, out=torch.empty(1, device=dev), ws=ws)
+    t_f = timed(lambda: ex.dot(x, y, out=r, ws=ws), nreps=3) if ex else None
+    rf = ex.dot(x, y, out=torch.empty(1, device=dev), ws=ws) if ex else None
     t_n = timed(lambda: ldist.sharded_dot(x, y, group, out=r, ws=ws), nreps=3)
     rn = ldist.sharded_dot(x, y, group, out=torch.empty(1, device=dev), ws=ws)
     del x, y
@@ -610,19 +650,23 @@ def scaling_configs(args, lift, ldist, gen, torch, dist, world, rank, dev, group
         del xf, yf5, wsf
     barrier()
     c5 = {"elements_per_rank": a1 - a0}
+    if not ex:
+        c5["fused"] = {"unavailable": ex_note}
     for k, t in (("kernel", t_k), ("fused", t_f), ("nccl", t_n)):
+        if t is None:
+            continue
         c5[k] = {"ms": round(t, 4), "GB/s": round(8 * NC5 / (t * 1e-3) / 1e9, 1),
                  "elements_per_s": float(f"{NC5 / (t * 1e-3):.4g}"),
                  "frac_of_8TBs_per_gpu": round(8 * NC5 / (t * 1e-3) / 1e9 / world / NOMINAL_HBM, 4)}
     if rank == 0:
         c5["t1_ms"] = round(ref["t1"], 4)
-        for k in ("kernel", "fused", "nccl"):
+        for k in paths:
             c5[k]["efficiency_vs_1"] = round(ref["t1"] / (world * c5[k]["ms"]), 4)
-        c5["bits_equal_unsharded"] = bool(torch.equal(rf.view(torch.int32), ref["bits"].view(torch.int32))
-                                          and torch.equal(rn.view(torch.int32),
-                                                          ref["bits"].view(torch.int32)))
+        c5["bits_equal_unsharded"] = bool(
+            (rf is None or torch.equal(rf.view(torch.int32), ref["bits"].view(torch.int32)))
+            and torch.equal(rn.view(torch.int32), ref["bits"].view(torch.int32)))
     out["C5 dot 2^31 sharded"] = c5
-    if xchg is None:
+    if xchg is None and ex is not None:
         ex.close()
     torch.cuda.empty_cache()
     return out
