@@ -234,7 +234,7 @@ size_t lift_gemv_workspace_bytes(int64_t m, int64_t n);
  *   (closed form; the paper does not print the helpers, P:825 — DESIGN.md reading R22).
  *   s: n floats in (prices > 0); call, put: n floats out (SoA).  fp32 arithmetic: N(-|d|)
  *   by the Abramowitz-Stegun 26.2.17 polynomial (|error| < 7.5e-8), log2/exp2/rcp by the
- *   hardware approximations (reading R22); per-option error <= 1e-6 (s + K)
+ *   hardware approximations (reading R22); per-option error <= 5e-7 (s + K)
  *   against the fp64 oracle.  K, v, T must be > 0 and finite, r finite, else
  *   LIFT_ERR_INVALID_VALUE.  n == 0 launches nothing. */
 lift_status lift_blackscholes(int64_t n, const float* s, float K, float r, float v, float T,

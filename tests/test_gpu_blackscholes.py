@@ -1,6 +1,6 @@
 """NEXT-3 row: BlackScholes (Fig. 9) on the GPU vs the fp64 oracle.
 
-Bar (reading R22): per option |g - o| <= 1e-6 * (s + K) — fp32
+Bar (reading R22): per option |g - o| <= 5e-7 * (s + K) — fp32
 arithmetic on prices bounded by s (call) and K (put); relative error is meaningless for
 deep out-of-the-money prices near 0.  Put-call parity holds on the GPU results to the
 same bound; any alignment gives the same bits."""
@@ -34,9 +34,9 @@ def test_blackscholes_vs_oracle(lift, n):
     scale = s.astype(np.float64) + K
     ec = np.abs(c.cpu().numpy() - oc) / scale
     ep = np.abs(p.cpu().numpy() - op) / scale
-    assert ec.max() <= 1e-6 and ep.max() <= 1e-6, (ec.max(), ep.max())
+    assert ec.max() <= 5e-7 and ep.max() <= 5e-7, (ec.max(), ep.max())
     par = c.cpu().numpy().astype(np.float64) - p.cpu().numpy() - (s - K * np.exp(-R * T))
-    assert np.abs(par / scale).max() <= 2e-6
+    assert np.abs(par / scale).max() <= 1e-6
 
 
 @pytest.mark.parametrize("params", [(40.0, 0.0, 0.6, 0.25), (15.0, 0.1, 0.05, 5.0),
@@ -47,8 +47,8 @@ def test_blackscholes_other_params(lift, params):
     c, p = lift.blackscholes(torch.from_numpy(s).to(DEV), k, r, v, t)
     oc, op = oracle.blackscholes(s, k, r, v, t)
     scale = s.astype(np.float64) + k
-    assert (np.abs(c.cpu().numpy() - oc) / scale).max() <= 1e-6
-    assert (np.abs(p.cpu().numpy() - op) / scale).max() <= 1e-6
+    assert (np.abs(c.cpu().numpy() - oc) / scale).max() <= 5e-7
+    assert (np.abs(p.cpu().numpy() - op) / scale).max() <= 5e-7
 
 
 def test_blackscholes_textbook(lift):
@@ -85,5 +85,5 @@ def test_blackscholes_extreme_moneyness(lift):
     assert np.all(np.isfinite(c)) and np.all(np.isfinite(p))
     oc, op = oracle.blackscholes(s, K, R, V, T)
     scale = s.astype(np.float64) + K
-    assert (np.abs(c - oc) / scale).max() <= 1e-6 and (np.abs(p - op) / scale).max() <= 1e-6
+    assert (np.abs(c - oc) / scale).max() <= 5e-7 and (np.abs(p - op) / scale).max() <= 5e-7
     assert c[0] == 0.0 and abs(p[0] - K * np.exp(-R * T)) <= 1e-4
