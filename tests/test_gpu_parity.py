@@ -589,3 +589,36 @@ def test_workspace_reset_restores_the_contract(lift):
         ws.buf[t0 + 4 * k:t0 + 4 * k + 4].view(torch.int32).fill_(1)
         assert not ws.check()
         ws.reset()
+
+
+# ---------------- accuracy beyond the bar: one fp32 rounding of an fp64-exact fold
+def _ulp32(o):
+    """The spacing of fp32 values at |o| (np.spacing of the fp32 rounding of o)."""
+    return np.abs(np.spacing(np.abs(np.asarray(o, dtype=np.float64)).astype(np.float32))).astype(np.float64)
+
+
+@pytest.mark.parametrize("op,n,lo", [("asum", 1 << 24, -1.0), ("dot", 1 << 26, -1.0),
+                                     ("dot", 1 << 24, 0.0), ("asum", (1 << 22) + 77, -1.0)])
+def test_reductions_within_one_fp32_ulp(lift, op, n, lo):
+    """The kernels fold in fp64 (exact products for dot) and round once (reading R13), so
+    their result is within one fp32 ulp of the fp64 oracle — far inside BASELINE's 1e-5 —
+    signed inputs included."""
+    xh = gen.host(n, 11, gen.TID_X, lo=lo, hi=1.0)
+    if op == "asum":
+        g, o = lift.asum(dev(xh)).item(), oracle.asum(xh)
+    else:
+        yh = gen.host(n, 11, gen.TID_Y, lo=lo, hi=2.0)
+        g, o = lift.dot(dev(xh), dev(yh)).item(), oracle.dot(xh, yh)
+    assert abs(g - o) <= _ulp32(o), (g, o)
+
+
+@pytest.mark.parametrize("m,n,alpha,beta,lo", [(4096, 4096, 1.5, 0.5, 0.0), (1000, 8192, -1.25, 0.75, -1.0)])
+def test_gemv_within_one_fp32_ulp(lift, m, n, alpha, beta, lo):
+    """Every gemv element within one fp32 ulp of the oracle (exact products, fp64 row
+    folds, the epilogue in fp64 rounded once: reading R10/R13)."""
+    A = gen.host(m * n, 12, gen.TID_A, lo=lo, hi=3.0).reshape(m, n)
+    x = gen.host(n, 12, gen.TID_X, lo=lo, hi=1.0)
+    y = gen.host(m, 12, gen.TID_Y, lo=lo, hi=2.0)
+    got = lift.gemv(dev(A), dev(x), dev(y), alpha, beta).cpu().numpy().astype(np.float64)
+    ref = oracle.gemv(A, x, y, alpha, beta)
+    assert np.all(np.abs(got - ref) <= _ulp32(ref))
