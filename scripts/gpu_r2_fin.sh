@@ -1,5 +1,7 @@
 #!/bin/bash
 # A/B of the reductions' completion schemes: in-tree build vs build/var_*.so (ab.py, midsize_ab.py, step_ab.py).
+# (Used for the designated-finisher, next-wave-prefetch and tagged-partial experiments, whose
+# kernel code was measured slower and not kept in the tree.)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 if [ -z "$SKIP_TESTS" ]; then
